@@ -1,0 +1,199 @@
+/*
+ * mc.h — C ABI of the B200 meshlet-compression library (libmc.so).
+ *
+ * The hot path of arXiv 2404.06359 "Towards Practical Meshlet Compression":
+ * per-meshlet decompression of generalized-triangle-strip topology
+ * (PAPER §4.2–4.3) and crack-free fixed-point attributes
+ * (PAPER §4.4) into plain index and vertex buffers,
+ * plus the host encoder that produces the stream.  The byte format is
+ * FORMAT.md (normative).  P:n cites PAPER.md line n, S:n SPEC.md line n.
+ *
+ * Conventions
+ *  - Plain C, no C++ types or exceptions cross this boundary; no torch types.
+ *  - "host" pointers are CPU memory, "device" pointers CUDA device memory.
+ *    Device buffers are always caller-owned (the Python binding allocates them
+ *    with torch); the decode path allocates no device memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Decode calls are asynchronous on `stream` and never synchronise the host.
+ *    Argument errors are detected synchronously and returned as mc_status;
+ *    malformed stream CONTENT is detected on the device and reported in
+ *    mc_stats.error_bits (FORMAT.md §5) — the kernel never traps and never
+ *    reads or writes outside the blob and the record's own output ranges.
+ *  - Every function is thread-safe; mc_blob objects are immutable once built.
+ */
+#ifndef MC_H
+#define MC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MC_OK = 0,
+    MC_ERR_ARG = 1,      /* NULL / inconsistent argument                                  */
+    MC_ERR_LIMITS = 2,   /* Ṽ, T̃ outside [3,256]/[1,256], n outside [1,16], b outside [1,24] */
+    MC_ERR_INPUT = 3,    /* bad source mesh: index >= V or a degenerate triangle    */
+    MC_ERR_FORMAT = 4,   /* bad magic/version/offsets: not a FORMAT.md blob        */
+    MC_ERR_RANGE = 5,    /* a grid index or an output count exceeds 32 bits                */
+    MC_ERR_CUDA = 6,     /* a CUDA runtime call failed                                     */
+    MC_ERR_NOMEM = 7     /* host allocation failed                                         */
+} mc_status;
+
+enum { MC_CODEC_GTS = 1, MC_CODEC_GTS_REUSE = 2 };              /* P:420–422 / P:423–426 */
+enum { MC_SEM_GENERIC = 0, MC_SEM_POSITION = 1, MC_SEM_NORMAL = 2, MC_SEM_TEXCOORD = 3,
+       MC_SEM_NORMAL_OCT = 4 /* one of two consecutive octahedral channels, FORMAT.md §4.3 */ };
+
+/* FORMAT.md §5 device error bits (mc_stats.error_bits) */
+enum { MC_DERR_RECORD = 1, MC_DERR_COUNTS = 2, MC_DERR_INDEX = 4, MC_DERR_REUSE = 8, MC_DERR_OBJECT = 16 };
+
+/* decode flags */
+enum {
+    MC_DECODE_BLOB_LOCAL_INDICES = 1  /* index value = vtx_base - base_vtx + local (shard-local
+                                         vertex buffer) instead of the global vtx_base + local */
+};
+
+/* ------------------------------------------------------------------ source mesh
+ * The paper's input: an indexed triangle list and per-vertex
+ * attribute vectors of n channels, with b_c bits per channel.
+ * All arrays are host memory, borrowed for the duration of mc_encode. */
+typedef struct {
+    uint32_t num_vertices;               /* V_src                                     */
+    uint32_t num_triangles;              /* T_src                                     */
+    const uint32_t *indices;             /* [3*T_src], winding as authored            */
+    const float *attributes;             /* [V_src*n], vertex-major                   */
+    uint32_t num_channels;               /* n, 1..16                                  */
+    const uint8_t *bits;                 /* [n], b_c in 1..24                         */
+    const uint8_t *semantic;             /* [n], MC_SEM_*                             */
+    const uint32_t *object_of_triangle;  /* [T_src] or NULL: one quantisation grid per
+                                            object (a mesh of a scene); meshlets never
+                                            cross objects                             */
+} mc_mesh;
+
+typedef struct {
+    uint32_t max_vertices;   /* Ṽ (the paper uses 128)                          */
+    uint32_t max_triangles;  /* T̃, bounds T' = T + 4R (the paper uses 256)       */
+    uint32_t codec;          /* MC_CODEC_*                                              */
+    uint32_t num_threads;    /* host worker threads, 0 = hardware concurrency           */
+} mc_encode_params;
+
+typedef struct mc_blob mc_blob;   /* opaque, library-owned, immutable host object */
+
+/* Parsed BlobHeader (FORMAT.md §1.1) plus derived sizes. */
+typedef struct {
+    uint32_t codec, n, n_out, S;          /* n_out = floats per output vertex, S = Σ b_c   */
+    uint32_t num_meshlets, num_objects, v_max, t_max;
+    uint32_t total_v, total_tp, total_t;  /* Σ V, Σ T' (decoded), Σ T (real)             */
+    uint32_t base_meshlet, base_vtx, base_tri, max_record_bytes;
+    uint64_t off_dir, off_obj, off_rec, total_bytes;
+    uint8_t bits[16], semantic[16];
+} mc_layout;
+
+/* Encode a mesh (P:279–305 meshlets; P:312–467 strips; P:486–492 quantisation).
+ * Meshlets are built under V <= Ṽ and T' <= T̃ (split when restarts overflow,
+ * P:453), stripified, re-labelled so new vertices appear in ascending order
+ * (P:456), and quantised on per-object global grids.  *out is owned by the
+ * caller until mc_blob_free.  Errors: MC_ERR_ARG, MC_ERR_LIMITS, MC_ERR_INPUT,
+ * MC_ERR_RANGE, MC_ERR_NOMEM. */
+mc_status mc_encode(const mc_mesh *mesh, const mc_encode_params *params, mc_blob **out);
+
+/* Instanced scene (BASELINE cfg4): for each instance i, copy every meshlet of
+ * protos[proto_of_instance[i]] with translated position-channel origins
+ * (offset[3*i..]).  Each instance's records are distinct bytes in the output.
+ * Output vertices/triangles are numbered instance after instance. */
+mc_status mc_blob_instance(const mc_blob *const *protos, uint32_t num_protos,
+                           const uint32_t *proto_of_instance, const float *offset,
+                           uint32_t num_instances, mc_blob **out);
+
+/* Wrap a copy of external FORMAT.md bytes (e.g. another encoder's output). */
+mc_status mc_blob_from_bytes(const void *bytes, size_t n, mc_blob **out);
+
+/* Borrow the serialised bytes (valid until mc_blob_free). */
+mc_status mc_blob_bytes(const mc_blob *blob, const void **bytes, size_t *n);
+
+/* For encoder-made blobs: the source vertex of every output vertex slot [total_v]
+ * and the source triangle of every decoded triangle slot [total_tp]
+ * (UINT32_MAX = restart degenerate).  MC_ERR_ARG if the blob has no map. */
+mc_status mc_blob_source_map(const mc_blob *blob, const uint32_t **src_vertex, const uint32_t **src_tri);
+
+/* Encoder statistics: restarts, meshlets split off because T' overflowed. */
+mc_status mc_blob_encode_stats(const mc_blob *blob, uint64_t *restarts, uint64_t *split_meshlets);
+
+void mc_blob_free(mc_blob *blob);
+
+/* Parse and validate a BlobHeader from host bytes. */
+mc_status mc_parse_header(const void *bytes, size_t n, mc_layout *out);
+
+/* Split records [0, M) into `parts` contiguous ranges with balanced algorithmic
+ * bytes (record bytes read + output bytes written); first[parts], count[parts]. */
+mc_status mc_blob_shard_ranges(const void *bytes, size_t n, uint32_t parts, uint32_t *first,
+                               uint32_t *count);
+
+/* Copy records [first, first+count) into a standalone blob whose base_* fields
+ * carry the range's original bases (checksums stay global, FORMAT.md §6). */
+mc_status mc_blob_extract(const void *bytes, size_t n, uint32_t first, uint32_t count,
+                          mc_blob **out);
+
+/* ------------------------------------------------------------------ device decode */
+typedef struct {
+    const mc_layout *layout;   /* host: mc_parse_header of the same blob                 */
+    const void *d_blob;        /* device: the blob bytes (16-B aligned base)              */
+    uint32_t first, count;     /* records [first, first+count) of this blob               */
+    uint32_t *d_indices;       /* device, required: 3*total_tp u32, FORMAT.md §2
+                                  (positions relative to base_tri of the blob)            */
+    float *d_vertices;         /* device or NULL: n_out*total_v fp32, FORMAT.md §4.2       */
+    uint32_t *d_quantized;     /* device or NULL: n*total_v u32 grid values, §4.1          */
+    uint32_t flags;            /* MC_DECODE_*                                             */
+} mc_decode_args;
+
+/* Device statistics (FORMAT.md §5, §6), accumulated atomically. */
+typedef struct {
+    uint64_t checksum_indices;     /* Σ mix64(k<<32 | word) over index words              */
+    uint64_t checksum_vertices;    /* same over fp32 vertex words (bit patterns)          */
+    uint64_t checksum_quantized;   /* same over quantised words                           */
+    uint64_t triangles;            /* Σ T' decoded                                        */
+    uint64_t degenerate;           /* decoded triangles with a repeated index             */
+    uint64_t vertices;             /* Σ V                                                 */
+    uint64_t multiword_lookbacks;  /* triangles whose L/R search crossed a word   */
+    uint32_t max_lookback;         /* max over triangles of t - j(t)                      */
+    uint32_t error_bits;           /* OR of FORMAT.md §5 bits                             */
+    uint32_t first_bad_meshlet;    /* smallest malformed record index, UINT32_MAX if none */
+    uint32_t num_bad;              /* malformed records                                   */
+} mc_stats;
+
+/* Decode records into the output buffers (the timed hot path).  One warp per
+ * meshlet, records staged into shared memory with TMA bulk copies. */
+mc_status mc_decode_meshlets(const mc_decode_args *args, void *stream);
+
+/* Same decode, additionally accumulating mc_stats into *d_stats (device). */
+mc_status mc_decode_stats(const mc_decode_args *args, mc_stats *d_stats, void *stream);
+
+/* Initialise a device mc_stats: zeros, first_bad_meshlet = UINT32_MAX. */
+mc_status mc_stats_reset(mc_stats *d_stats, void *stream);
+
+/* End-to-end decode from HOST buffers: H2D of the blob, decode, D2H of the
+ * outputs, all enqueued on `stream` (host buffers should be pinned for overlap).
+ * Device buffers are caller-owned scratch of the sizes mc_decode_args states. */
+typedef struct {
+    const mc_layout *layout;
+    const void *h_blob;        /* host: total_bytes                                       */
+    void *d_blob;              /* device scratch: >= total_bytes                          */
+    uint32_t *h_indices;       /* host out: 3*total_tp                                     */
+    float *h_vertices;         /* host out or NULL                                        */
+    uint32_t *h_quantized;     /* host out or NULL                                        */
+    uint32_t *d_indices;       /* device scratch                                           */
+    float *d_vertices;         /* device scratch or NULL (NULL iff h_vertices NULL)       */
+    uint32_t *d_quantized;     /* device scratch or NULL                                   */
+    uint32_t flags;
+} mc_host_decode_args;
+mc_status mc_decode_host(const mc_host_decode_args *args, void *stream);
+
+const char *mc_status_str(mc_status s);
+uint32_t mc_abi_version(void);   /* 1 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MC_H */

@@ -208,6 +208,9 @@ uint32_t or_decode_meshlet(const uint8_t *blob, size_t nbytes, uint32_t m, uint3
         for (uint32_t t = 1; t < Tp; ++t) total += get_bit(INC, t);
         if (total != V - 3u) err |= DERR_COUNTS;
     }
+    /* structural errors (RECORD/COUNTS/OBJECT) end the record: FORMAT.md §5 evaluates
+     * INDEX/REUSE only for structurally valid records */
+    if (err) return err;
     uint32_t c = 0; /* inclusive add-scan of increment flags over triangles 1..t */
     for (uint32_t t = 1; t < Tp; ++t) {
         uint32_t w;
@@ -291,12 +294,11 @@ uint32_t or_decode_range(const uint8_t *blob, size_t nbytes, uint32_t m0, uint32
         uint32_t e = or_decode_meshlet(blob, nbytes, m, tri, q ? qq : NULL, f ? ff : NULL, meta);
         if (err_out) err_out[m - m0] = e;
         all |= e;
-        if (e & DERR_RECORD) continue;
+        if (e & (DERR_RECORD | DERR_COUNTS | DERR_OBJECT)) continue;
         uint32_t V = meta[2], Tp = meta[3];
         uint64_t tb = (uint64_t)meta[1] - h.base_tri, vb = (uint64_t)meta[0] - h.base_vtx;
         if (tb + Tp > h.total_tp || vb + V > h.total_v) { if (err_out) err_out[m - m0] |= DERR_RECORD; all |= DERR_RECORD; continue; }
         for (uint32_t k = 0; k < 3 * Tp; ++k) idx[3 * tb + k] = meta[0] + tri[k];
-        if (e & (DERR_OBJECT | DERR_COUNTS)) continue;
         if (q) memcpy(q + vb * h.n, qq, 4ull * V * h.n);
         if (f) memcpy(f + vb * h.n_out, ff, 4ull * V * h.n_out);
     }

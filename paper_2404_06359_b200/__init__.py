@@ -1,0 +1,296 @@
+"""B200-native meshlet decompression (arXiv 2404.06359) — thin Python binding of libmc.so.
+
+Every step of the hot path runs in the C-ABI library (``include/mc.h``): the host
+encoder in C++, the decoder in hand-written sm_100a CUDA.  This module only marshals
+arguments (numpy host arrays, torch device tensors, CUDA stream handles).  There is
+no Python or CPU fallback: if ``libmc.so`` is missing, importing the binding fails.
+
+Function names follow the C ABI: ``mc_encode``, ``mc_decode_meshlets``,
+``mc_decode_stats``, ``mc_decode_host``, ``mc_blob_instance``, ...
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+LIB_PATH = _build.LIB
+
+MC_CODEC_GTS, MC_CODEC_GTS_REUSE = 1, 2
+MC_DECODE_BLOB_LOCAL_INDICES = 1
+MC_DERR_RECORD, MC_DERR_COUNTS, MC_DERR_INDEX, MC_DERR_REUSE, MC_DERR_OBJECT = 1, 2, 4, 8, 16
+
+
+class MCError(RuntimeError):
+    pass
+
+
+class mc_layout(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in
+                ("codec", "n", "n_out", "S", "num_meshlets", "num_objects", "v_max", "t_max",
+                 "total_v", "total_tp", "total_t", "base_meshlet", "base_vtx", "base_tri", "max_record_bytes")] + \
+               [("off_dir", ctypes.c_uint64), ("off_obj", ctypes.c_uint64), ("off_rec", ctypes.c_uint64),
+                ("total_bytes", ctypes.c_uint64), ("bits", ctypes.c_uint8 * 16), ("semantic", ctypes.c_uint8 * 16)]
+
+
+class mc_mesh(ctypes.Structure):
+    _fields_ = [("num_vertices", ctypes.c_uint32), ("num_triangles", ctypes.c_uint32),
+                ("indices", ctypes.c_void_p), ("attributes", ctypes.c_void_p),
+                ("num_channels", ctypes.c_uint32), ("bits", ctypes.c_void_p), ("semantic", ctypes.c_void_p),
+                ("object_of_triangle", ctypes.c_void_p)]
+
+
+class mc_encode_params(ctypes.Structure):
+    _fields_ = [("max_vertices", ctypes.c_uint32), ("max_triangles", ctypes.c_uint32),
+                ("codec", ctypes.c_uint32), ("num_threads", ctypes.c_uint32)]
+
+
+class mc_decode_args(ctypes.Structure):
+    _fields_ = [("layout", ctypes.POINTER(mc_layout)), ("d_blob", ctypes.c_void_p),
+                ("first", ctypes.c_uint32), ("count", ctypes.c_uint32),
+                ("d_indices", ctypes.c_void_p), ("d_vertices", ctypes.c_void_p),
+                ("d_quantized", ctypes.c_void_p), ("flags", ctypes.c_uint32)]
+
+
+class mc_host_decode_args(ctypes.Structure):
+    _fields_ = [("layout", ctypes.POINTER(mc_layout)), ("h_blob", ctypes.c_void_p), ("d_blob", ctypes.c_void_p),
+                ("h_indices", ctypes.c_void_p), ("h_vertices", ctypes.c_void_p), ("h_quantized", ctypes.c_void_p),
+                ("d_indices", ctypes.c_void_p), ("d_vertices", ctypes.c_void_p), ("d_quantized", ctypes.c_void_p),
+                ("flags", ctypes.c_uint32)]
+
+
+class mc_stats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint64) for k in
+                ("checksum_indices", "checksum_vertices", "checksum_quantized", "triangles", "degenerate",
+                 "vertices", "multiword_lookbacks")] + \
+               [(k, ctypes.c_uint32) for k in ("max_lookback", "error_bits", "first_bad_meshlet", "num_bad")]
+
+
+STATS_BYTES = ctypes.sizeof(mc_stats)
+EXPORTS = ["mc_encode", "mc_blob_instance", "mc_blob_from_bytes", "mc_blob_bytes", "mc_blob_source_map",
+           "mc_blob_encode_stats", "mc_blob_free", "mc_parse_header", "mc_blob_shard_ranges", "mc_blob_extract",
+           "mc_decode_meshlets", "mc_decode_stats", "mc_stats_reset", "mc_decode_host", "mc_status_str",
+           "mc_abi_version"]
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libmc.so (built in-tree by ``__graft_entry__.build()``); fail loudly if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, u32, sz = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_size_t
+        for name in EXPORTS:
+            getattr(L, name).restype = ctypes.c_int
+        L.mc_status_str.restype = ctypes.c_char_p
+        L.mc_abi_version.restype = u32
+        L.mc_encode.argtypes = [ctypes.POINTER(mc_mesh), ctypes.POINTER(mc_encode_params), ctypes.POINTER(P)]
+        L.mc_blob_instance.argtypes = [P, u32, P, P, u32, ctypes.POINTER(P)]
+        L.mc_blob_from_bytes.argtypes = [P, sz, ctypes.POINTER(P)]
+        L.mc_blob_bytes.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(sz)]
+        L.mc_blob_source_map.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P)]
+        L.mc_blob_encode_stats.argtypes = [P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+        L.mc_blob_free.argtypes = [P]
+        L.mc_blob_free.restype = None
+        L.mc_parse_header.argtypes = [P, sz, ctypes.POINTER(mc_layout)]
+        L.mc_blob_shard_ranges.argtypes = [P, sz, u32, P, P]
+        L.mc_blob_extract.argtypes = [P, sz, u32, u32, ctypes.POINTER(P)]
+        L.mc_decode_meshlets.argtypes = [ctypes.POINTER(mc_decode_args), P]
+        L.mc_decode_stats.argtypes = [ctypes.POINTER(mc_decode_args), P, P]
+        L.mc_stats_reset.argtypes = [P, P]
+        L.mc_decode_host.argtypes = [ctypes.POINTER(mc_host_decode_args), P]
+        L.mc_status_str.argtypes = [ctypes.c_int]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise MCError(f"{what}: {lib().mc_status_str(rc).decode()} (status {rc})")
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ----------------------------------------------------------------------------- blobs
+
+class Blob:
+    """An encoded meshlet stream (FORMAT.md) owned by libmc (``mc_blob``)."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self._h = handle
+        bp, n = ctypes.c_void_p(), ctypes.c_size_t()
+        _check(lib().mc_blob_bytes(self._h, ctypes.byref(bp), ctypes.byref(n)), "mc_blob_bytes")
+        self.bytes = np.ctypeslib.as_array(ctypes.cast(bp, ctypes.POINTER(ctypes.c_uint8)), (n.value,))
+        self.layout = parse_header(self.bytes)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.mc_blob_free(h)
+            self._h = None
+
+    @classmethod
+    def from_bytes(cls, data: np.ndarray) -> "Blob":
+        data = np.ascontiguousarray(data, dtype=np.uint8)
+        h = ctypes.c_void_p()
+        _check(lib().mc_blob_from_bytes(_p(data), data.nbytes, ctypes.byref(h)), "mc_blob_from_bytes")
+        return cls(h)
+
+    def source_map(self):
+        sv, st = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib().mc_blob_source_map(self._h, ctypes.byref(sv), ctypes.byref(st)), "mc_blob_source_map")
+        L = self.layout
+        v = np.ctypeslib.as_array(ctypes.cast(sv, ctypes.POINTER(ctypes.c_uint32)), (max(L.total_v, 1),))[:L.total_v]
+        t = np.ctypeslib.as_array(ctypes.cast(st, ctypes.POINTER(ctypes.c_uint32)), (max(L.total_tp, 1),))[:L.total_tp]
+        return v.copy(), t.copy()
+
+    def encode_stats(self):
+        r, s = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().mc_blob_encode_stats(self._h, ctypes.byref(r), ctypes.byref(s)), "mc_blob_encode_stats")
+        return {"restarts": r.value, "split_meshlets": s.value}
+
+    def shard_ranges(self, parts: int):
+        return mc_blob_shard_ranges(self.bytes, parts)
+
+    def extract(self, first: int, count: int) -> "Blob":
+        return mc_blob_extract(self.bytes, first, count)
+
+
+def parse_header(data: np.ndarray) -> mc_layout:
+    L = mc_layout()
+    _check(lib().mc_parse_header(_p(data), data.nbytes, ctypes.byref(L)), "mc_parse_header")
+    return L
+
+
+def mc_encode(mesh, max_vertices: int = 64, max_triangles: int = 126, codec: int = MC_CODEC_GTS_REUSE,
+              num_threads: int = 0) -> Blob:
+    """Encode a mesh (any object with indices/attributes/bits/semantic[/object_of_triangle])."""
+    idx = np.ascontiguousarray(mesh.indices, dtype=np.uint32)
+    attr = np.ascontiguousarray(mesh.attributes, dtype=np.float32)
+    bits = np.ascontiguousarray(np.asarray(mesh.bits, dtype=np.uint8))
+    sem = np.ascontiguousarray(np.asarray(mesh.semantic, dtype=np.uint8))
+    obj = getattr(mesh, "object_of_triangle", None)
+    obj = None if obj is None else np.ascontiguousarray(obj, dtype=np.uint32)
+    m = mc_mesh(attr.shape[0], idx.reshape(-1, 3).shape[0], _p(idx), _p(attr), attr.shape[1], _p(bits), _p(sem),
+                _p(obj))
+    prm = mc_encode_params(max_vertices, max_triangles, codec, num_threads)
+    h = ctypes.c_void_p()
+    _check(lib().mc_encode(ctypes.byref(m), ctypes.byref(prm), ctypes.byref(h)), "mc_encode")
+    return Blob(h)
+
+
+def mc_blob_instance(protos, proto_of_instance, offsets) -> Blob:
+    arr = (ctypes.c_void_p * len(protos))(*[p._h.value for p in protos])
+    pi = np.ascontiguousarray(proto_of_instance, dtype=np.uint32)
+    off = np.ascontiguousarray(offsets, dtype=np.float32).reshape(-1)
+    h = ctypes.c_void_p()
+    _check(lib().mc_blob_instance(ctypes.cast(arr, ctypes.c_void_p), len(protos), _p(pi), _p(off), pi.size,
+                                  ctypes.byref(h)), "mc_blob_instance")
+    return Blob(h)
+
+
+def mc_blob_shard_ranges(data: np.ndarray, parts: int):
+    first = np.zeros(parts, np.uint32)
+    count = np.zeros(parts, np.uint32)
+    _check(lib().mc_blob_shard_ranges(_p(data), data.nbytes, parts, _p(first), _p(count)), "mc_blob_shard_ranges")
+    return [(int(f), int(c)) for f, c in zip(first, count)]
+
+
+def mc_blob_extract(data: np.ndarray, first: int, count: int) -> Blob:
+    h = ctypes.c_void_p()
+    _check(lib().mc_blob_extract(_p(data), data.nbytes, first, count, ctypes.byref(h)), "mc_blob_extract")
+    return Blob(h)
+
+
+# ----------------------------------------------------------------------------- device decode
+
+def _tptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_handle(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def mc_decode_meshlets(layout: mc_layout, d_blob, d_indices, d_vertices=None, d_quantized=None, first: int = 0,
+                       count: int | None = None, flags: int = 0, stream=None):
+    """Enqueue the decode of records [first, first+count) on `stream` (torch stream or None)."""
+    count = layout.num_meshlets - first if count is None else count
+    a = mc_decode_args(ctypes.pointer(layout), d_blob.data_ptr(), first, count, d_indices.data_ptr(),
+                       None if d_vertices is None else d_vertices.data_ptr(),
+                       None if d_quantized is None else d_quantized.data_ptr(), flags)
+    _check(lib().mc_decode_meshlets(ctypes.byref(a), _stream_handle(stream)), "mc_decode_meshlets")
+
+
+def mc_stats_reset(d_stats, stream=None):
+    _check(lib().mc_stats_reset(_tptr(d_stats), _stream_handle(stream)), "mc_stats_reset")
+
+
+def mc_decode_stats(layout: mc_layout, d_blob, d_indices, d_stats, d_vertices=None, d_quantized=None, first: int = 0,
+                    count: int | None = None, flags: int = 0, stream=None):
+    count = layout.num_meshlets - first if count is None else count
+    a = mc_decode_args(ctypes.pointer(layout), d_blob.data_ptr(), first, count, d_indices.data_ptr(),
+                       None if d_vertices is None else d_vertices.data_ptr(),
+                       None if d_quantized is None else d_quantized.data_ptr(), flags)
+    _check(lib().mc_decode_stats(ctypes.byref(a), _tptr(d_stats), _stream_handle(stream)), "mc_decode_stats")
+
+
+def read_stats(d_stats) -> dict:
+    """Copy a device mc_stats (a uint8 tensor of STATS_BYTES) to a dict (synchronises)."""
+    raw = d_stats.cpu().numpy().tobytes()
+    s = mc_stats.from_buffer_copy(raw)
+    return {k: getattr(s, k) for k, _ in mc_stats._fields_}
+
+
+def mc_decode_host(layout: mc_layout, h_blob, d_blob, h_indices, d_indices, h_vertices=None, d_vertices=None,
+                   h_quantized=None, d_quantized=None, flags: int = 0, stream=None):
+    """End-to-end decode from host tensors (pinned for overlap): H2D, decode, D2H on `stream`."""
+    a = mc_host_decode_args(ctypes.pointer(layout), h_blob.data_ptr(), d_blob.data_ptr(), h_indices.data_ptr(),
+                            None if h_vertices is None else h_vertices.data_ptr(),
+                            None if h_quantized is None else h_quantized.data_ptr(), d_indices.data_ptr(),
+                            None if d_vertices is None else d_vertices.data_ptr(),
+                            None if d_quantized is None else d_quantized.data_ptr(), flags)
+    _check(lib().mc_decode_host(ctypes.byref(a), _stream_handle(stream)), "mc_decode_host")
+
+
+class DeviceBlob:
+    """A blob resident in HBM plus output buffers sized from its layout (torch tensors)."""
+
+    def __init__(self, blob, device="cuda", want_vertices=True, want_quantized=False):
+        import torch
+        data = blob.bytes if isinstance(blob, Blob) else np.ascontiguousarray(blob, dtype=np.uint8)
+        self.layout = parse_header(data)
+        L = self.layout
+        self.d_blob = torch.from_numpy(np.array(data, copy=True)).to(device)
+        self.indices = torch.empty(3 * L.total_tp, dtype=torch.int32, device=device)
+        self.vertices = torch.empty(L.n_out * L.total_v, dtype=torch.float32, device=device) if want_vertices else None
+        self.quantized = torch.empty(L.n * L.total_v, dtype=torch.int32, device=device) if want_quantized else None
+        self.stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=device)
+
+    def decode(self, stream=None, flags=0, first=0, count=None):
+        mc_decode_meshlets(self.layout, self.d_blob, self.indices, self.vertices, self.quantized, first, count,
+                           flags, stream)
+
+    def decode_stats(self, stream=None, flags=0, first=0, count=None) -> dict:
+        mc_stats_reset(self.stats, stream)
+        mc_decode_stats(self.layout, self.d_blob, self.indices, self.stats, self.vertices, self.quantized, first,
+                        count, flags, stream)
+        return read_stats(self.stats)
+
+    def algorithmic_bytes(self) -> int:
+        """Compressed bytes read (directory + records + object table) + decompressed bytes written."""
+        L = self.layout
+        read = (L.total_bytes - L.off_rec) + 4 * (L.num_meshlets + 1) + 8 * L.n * L.num_objects
+        write = 12 * L.total_tp + (4 * L.n_out * L.total_v if self.vertices is not None else 0) + \
+            (4 * L.n * L.total_v if self.quantized is not None else 0)
+        return int(read + write)

@@ -1,0 +1,699 @@
+// decode.cu — the hot path of libmc: per-meshlet decompression on sm_100a (B200).
+//
+// Paper: arXiv 2404.06359 §4.2–4.4.  One WARP decodes one meshlet record
+// (FORMAT.md) at a time and loops over records with a grid stride:
+//
+//   a1/a2  the record (header + L/R flags + increment flags + bytes + packed
+//          attributes) is staged HBM -> shared memory with ONE TMA 1-D bulk copy
+//          (cp.async.bulk ... mbarrier::complete_tx), double-buffered per warp so
+//          record i+1 is in flight while record i decodes;
+//   a3     index expansion: per-word __popc of the increment flags, an
+//          exclusive warp scan over <= 8 words (__shfl), then
+//          N[t+2] = i_t ? 2 + c_t : reuse[t - c_t - 1]      ("countbits");
+//   a4     L/R lookback by bit scan: j(t) = max{k<t: f_k != f_t} via
+//          31 - __clz((f_t ? ~w : w) & below(t)) over the current and earlier
+//          words ("firstbithigh", multi-word fallback);
+//   a5     triangle assembly with winding-preserving orientation (FORMAT.md §2);
+//   a6     index words staged in smem at the destination's 16-B phase, then
+//          written with coalesced 128-bit stores;
+//   a7/a8  attribute unpack by __funnelshift_r, q = L + code, fp32 via
+//          __fmaf_rn(__uint2float_rn(q), Δ, g), octahedral normals
+//          with IEEE-exact div/sqrt (FORMAT.md §4.3);
+//   a9     vertex words stored with 128-bit stores (direct when n_out % 4 == 0,
+//          else through the phase-aligned smem stage);
+//   a10    (stats kernel only) checksums/counters, warp-reduced, one atomic per warp.
+//
+// No tensor cores: the path is integer bit manipulation plus one FMA per
+// channel, bound by HBM bandwidth.  No --use_fast_math.
+#include "../../include/mc.h"
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+
+namespace {
+
+constexpr int kWarpsPerCta = 8;
+constexpr int kThreads = kWarpsPerCta * 32;
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr uint32_t kMiscWords = 112;   // 2 mbarriers, 2 sizes, 32 consts, N[272 B]
+
+struct Params {
+    const uint8_t* rec;        // records section
+    const uint32_t* dir;       // directory [M+1]
+    const float* objtab;       // object table [O][2n]
+    uint64_t rec_section_bytes;
+    uint32_t first, end;       // record range
+    uint32_t O, vmax, tmax, n, n_out, S, max_rec;
+    uint32_t base_vtx, base_tri, total_v, total_tp;
+    uint32_t index_sub;        // subtracted from index values (MC_DECODE_BLOB_LOCAL_INDICES)
+    uint32_t hdr_words;        // record header words (16 + 4n rounded to 16) / 4
+    uint32_t buf_words;        // per-buffer words (max_rec/4 + 4)
+    uint32_t idx_stage_words;  // 3*tmax + 8
+    uint32_t vtx_stage_words;  // vmax*n_out + 8 (0 when stores go direct)
+    uint32_t* idx;
+    float* fout;
+    uint32_t* qout;
+    mc_stats* stats;
+    uint8_t bits[16];
+    uint8_t bitoff[16];        // bit offset of channel c inside a vertex record
+    uint8_t col[16];           // output column of channel c (oct pair: column of n_x)
+    uint8_t oct[16];           // 1 on the first channel of an octahedral pair
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+// TMA 1-D bulk copy global -> shared, completion signalled on an mbarrier (tx bytes).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void st_v4(uint32_t* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xbf58476d1ce4e5b9ull;
+    z ^= z >> 27;
+    z *= 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    return z;
+}
+
+// Warp-cooperative store of `nwords` u32 from smem to global.  `src` was written at
+// the destination's 16-B phase: src[k] holds dst[k] and (src + head) is 16-B aligned.
+__device__ __forceinline__ void warp_store_words(uint32_t* dst, const uint32_t* src, uint32_t nwords, int lane) {
+    const uint32_t head = umin((4u - ((uint32_t)(reinterpret_cast<uintptr_t>(dst) >> 2) & 3u)) & 3u, nwords);
+    if ((uint32_t)lane < head) dst[lane] = src[lane];
+    const uint32_t body = (nwords - head) >> 2;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    uint32_t* d = dst + head;
+    for (uint32_t i = lane; i < body; i += 32) st_v4(d + 4 * i, s4[i]);
+    const uint32_t tail = (nwords - head) & 3u;
+    if ((uint32_t)lane < tail) d[4 * body + lane] = src[head + 4 * body + lane];
+}
+
+// FORMAT.md §4.3 octahedral decode, IEEE binary32 RN, no contraction.
+__device__ __forceinline__ void oct_decode(float ex, float ey, float& ox, float& oy, float& oz) {
+    const float ax = fabsf(ex), ay = fabsf(ey);
+    const float z = __fsub_rn(__fsub_rn(1.0f, ax), ay);
+    float x = ex, y = ey;
+    if (z < 0.0f) {
+        x = __fmul_rn(__fsub_rn(1.0f, ay), ex >= 0.0f ? 1.0f : -1.0f);
+        y = __fmul_rn(__fsub_rn(1.0f, ax), ey >= 0.0f ? 1.0f : -1.0f);
+    }
+    const float s2 = __fmaf_rn(z, z, __fmaf_rn(y, y, __fmul_rn(x, x)));
+    const float r = __fsqrt_rn(s2);
+    ox = __fdiv_rn(x, r);
+    oy = __fdiv_rn(y, r);
+    oz = __fdiv_rn(z, r);
+}
+
+struct WarpStats {
+    uint64_t cs_idx = 0, cs_f = 0, cs_q = 0, tris = 0, degen = 0, verts = 0, multi = 0;
+    uint32_t max_lb = 0;
+};
+
+// ------------------------------------------------------------------ the kernel
+// NCH > 0: compile-time channel count (register arrays, static indexing), OCT0 = first
+// channel of the octahedral pair or -1.  NCH == 0: generic runtime layout.
+template <int CODEC, bool STATS, int NCH, int OCT0>
+__global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_constant__ Params P) {
+    constexpr int NOUT = NCH > 0 ? NCH + (OCT0 >= 0 ? 1 : 0) : 1;
+    const uint32_t NOUT_RT = NCH > 0 ? (uint32_t)NOUT : P.n_out;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+
+    // per-warp smem carve-up (all offsets multiples of 16 B)
+    const uint32_t warp_words = 2 * P.buf_words + P.idx_stage_words + P.vtx_stage_words + kMiscWords;
+    uint32_t* wbase = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)wid * warp_words;
+    uint32_t* buf0 = wbase;
+    uint32_t* idx_stage = wbase + 2 * P.buf_words;
+    uint32_t* vtx_stage = idx_stage + P.idx_stage_words;
+    uint32_t* misc = vtx_stage + P.vtx_stage_words;                 // kMiscWords words
+    uint64_t* bars = reinterpret_cast<uint64_t*>(misc);               // 2 mbarriers (4 words)
+    uint32_t* sizes = misc + 4;                                       // staged size per buffer (2)
+    float* consts = reinterpret_cast<float*>(misc + 8);               // Δ[16], g[16]
+    uint8_t* Nbuf = reinterpret_cast<uint8_t*>(misc + 40);            // N[0..T'+1], 272 B
+
+    const uint32_t gwarp = blockIdx.x * kWarpsPerCta + wid;
+    const uint32_t nwarps = gridDim.x * kWarpsPerCta;
+    uint32_t m = P.first + gwarp;
+
+    if (lane == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+
+    // lane 0 issues the bulk copy of record `mm` into buffer `b` (or a plain arrive for a
+    // record that cannot be staged; its size is then recorded as 0 -> RECORD error)
+    auto issue = [&](uint32_t mm, uint32_t d0, uint32_t d1, int b) {
+        uint64_t off = 16ull * d0;
+        uint32_t bytes = (d1 > d0) ? 16u * (d1 - d0) : 0u;
+        bool ok = bytes != 0 && bytes <= P.max_rec && off + bytes <= P.rec_section_bytes;
+        sizes[b] = ok ? bytes : 0u;
+        if (ok) {
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&bars[b], bytes);
+            bulk_g2s(buf0 + (size_t)b * P.buf_words, P.rec + off, bytes, &bars[b]);
+        } else {
+            mbar_arrive(&bars[b]);
+        }
+    };
+
+    // directory prefetch: (d0,d1) for the next record to issue
+    uint32_t nd0 = 0, nd1 = 0;
+    if (m < P.end && lane == 0) {
+        uint32_t d0 = __ldg(P.dir + m), d1 = __ldg(P.dir + m + 1);
+        issue(m, d0, d1, 0);
+        if (m + nwarps < P.end) { nd0 = __ldg(P.dir + m + nwarps); nd1 = __ldg(P.dir + m + nwarps + 1); }
+    }
+
+    WarpStats ws;
+    uint32_t k = 0;
+    for (; m < P.end; m += nwarps, ++k) {
+        const int b = k & 1;
+        const uint32_t mnext = m + nwarps;
+        if (lane == 0 && mnext < P.end) {
+            issue(mnext, nd0, nd1, b ^ 1);
+            const uint32_t m2 = mnext + nwarps;
+            if (m2 < P.end) { nd0 = __ldg(P.dir + m2); nd1 = __ldg(P.dir + m2 + 1); }
+        }
+        mbar_wait(&bars[b], (k >> 1) & 1);
+        __syncwarp();
+        const uint32_t* R = buf0 + (size_t)b * P.buf_words;
+        const uint32_t staged = sizes[b];
+
+        // ---------------- a1: header (FORMAT.md §1.4)
+        const uint32_t vtx_base = R[0], tri_base = R[1], w2 = R[2];
+        const uint32_t V = (w2 & 0xFFu) + 1u, Tp = ((w2 >> 8) & 0xFFu) + 1u, object = w2 >> 16;
+        const uint32_t W = (Tp + 31u) >> 5;
+        const uint32_t nb = (CODEC == MC_CODEC_GTS) ? (Tp - 1u) : ((V >= 3u && V - 3u <= Tp - 1u) ? (Tp - 1u) - (V - 3u) : 0u);
+        const uint32_t lr_w = P.hdr_words;
+        const uint32_t inc_w = lr_w + W;
+        const uint32_t by_w = inc_w + (CODEC == MC_CODEC_GTS_REUSE ? W : 0u);
+        const uint32_t at_w = by_w + ((nb + 3u) >> 2);
+        const uint32_t need = ((at_w + ((V * P.S + 31u) >> 5)) * 4u + 15u) & ~15u;
+        uint32_t err = 0;
+        if (staged == 0 || need != staged) err |= MC_DERR_RECORD;
+        else {
+            if (V < 3u || V > P.vmax || Tp > P.tmax) err |= MC_DERR_COUNTS;
+            if (object >= P.O) err |= MC_DERR_OBJECT;
+            if ((uint64_t)tri_base - P.base_tri + Tp > P.total_tp || tri_base < P.base_tri ||
+                (uint64_t)vtx_base - P.base_vtx + V > P.total_v || vtx_base < P.base_vtx)
+                err |= MC_DERR_RECORD;
+        }
+        const uint32_t* LR = R + lr_w;
+        const uint32_t* INC = R + inc_w;
+        const uint8_t* BY = reinterpret_cast<const uint8_t*>(R + by_w);
+        const uint32_t* AT = R + at_w;
+
+        // ---------------- a3: increment-flag popcount prefix (GTS-Reuse)
+        uint32_t my_pc = 0, my_excl = 0;
+        if (CODEC == MC_CODEC_GTS_REUSE && !err) {
+            if ((uint32_t)lane < W) {
+                uint32_t w = INC[lane];
+                if (lane == 0) w &= ~1u;                                   // bit 0 ignored
+                const uint32_t rem = Tp - 32u * lane;
+                if (rem < 32u) w &= (1u << rem) - 1u;                       // bits >= T' ignored
+                my_pc = __popc(w);
+            }
+            uint32_t incl = my_pc;
+#pragma unroll
+            for (int d = 1; d < 8; d <<= 1) {
+                uint32_t o = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += o;
+            }
+            my_excl = incl - my_pc;
+            const uint32_t total = __shfl_sync(kFull, incl, 7);
+            if (total != V - 3u) err |= MC_DERR_COUNTS;
+        }
+        err = __shfl_sync(kFull, err, 0);
+        if (err) {
+            if (STATS && lane == 0) {
+                atomicOr(&P.stats->error_bits, err);
+                atomicMin(&P.stats->first_bad_meshlet, m);
+                atomicAdd(&P.stats->num_bad, 1u);
+            }
+            __syncwarp();
+            continue;
+        }
+
+        // N[0..2] = 0,1,2; N[t+2] for t = 1..T'-1
+        if (lane < 3) Nbuf[lane] = (uint8_t)lane;
+        uint32_t e2 = 0;
+        for (uint32_t j = 0; j < W; ++j) {
+            const uint32_t t = 32u * j + lane;
+            uint32_t wv = 0;
+            if (CODEC == MC_CODEC_GTS) {
+                if (t >= 1u && t < Tp) {
+                    wv = BY[t - 1u];
+                    if (wv >= V) e2 |= MC_DERR_INDEX;
+                }
+            } else {
+                uint32_t iw = INC[j];
+                if (j == 0) iw &= ~1u;
+                const uint32_t pre = __shfl_sync(kFull, my_excl, j);
+                if (t >= 1u && t < Tp) {
+                    const uint32_t i_t = (iw >> lane) & 1u;
+                    const uint32_t c = pre + __popc(iw & (0xFFFFFFFFu >> (31 - lane)));   // inclusive
+                    if (i_t) wv = 2u + c;
+                    else {
+                        wv = BY[t - c - 1u];                                // P:465 (t+1-s, s=2+c)
+                        if (wv >= V) e2 |= MC_DERR_REUSE;
+                    }
+                }
+            }
+            if (t >= 1u && t < Tp) Nbuf[t + 2u] = (uint8_t)wv;
+        }
+        __syncwarp();
+
+        // ---------------- a4/a5: L/R lookback + triangle assembly
+        const uint32_t vout = vtx_base - P.index_sub;
+        const uint32_t tpos = tri_base - P.base_tri;                        // output triangle position
+        uint32_t* idst = P.idx + 3ull * tpos;
+        const uint32_t iphase = (uint32_t)(reinterpret_cast<uintptr_t>(idst) >> 2) & 3u;
+        uint32_t* ist = idx_stage + iphase;
+        for (uint32_t j = 0; j < W; ++j) {
+            const uint32_t t = 32u * j + lane;
+            if (t < Tp) {
+                uint32_t a0, a1, a2;
+                if (t == 0) {
+                    a0 = 0; a1 = 1; a2 = 2;
+                } else {
+                    uint32_t lw = LR[j];
+                    if (j == 0) lw &= ~1u;                                  // f_0 := L
+                    const uint32_t f = (lw >> lane) & 1u;
+                    const uint32_t below = (1u << lane) - 1u;
+                    uint32_t x = (f ? ~lw : lw) & below;                    // differing flags below t
+                    int jj = -1;
+                    if (x) jj = (int)(32u * j) + 31 - __clz(x);
+                    else {
+                        // multi-word fallback: rare fans longer than the word
+                        for (int jp = (int)j - 1; jp >= 0; --jp) {
+                            uint32_t pw = LR[jp];
+                            if (jp == 0) pw &= ~1u;
+                            const uint32_t y = f ? ~pw : pw;
+                            if (y) { jj = 32 * jp + 31 - __clz(y); break; }
+                        }
+                        if (STATS && j > 0) ws.multi++;
+                    }
+                    const uint32_t nprev = Nbuf[t + 1u], npiv = Nbuf[jj + 1], nnew = Nbuf[t + 2u];
+                    if (f) { a0 = nprev; a1 = npiv; }                       // R: (N[t+1], N[j+1], N[t+2])
+                    else   { a0 = npiv;  a1 = nprev; }                      // L: (N[j+1], N[t+1], N[t+2])
+                    a2 = nnew;
+                    if (STATS) ws.max_lb = max(ws.max_lb, (uint32_t)((int)t - jj));
+                }
+                const uint32_t o0 = vout + a0, o1 = vout + a1, o2 = vout + a2;
+                ist[3 * t] = o0;
+                ist[3 * t + 1] = o1;
+                ist[3 * t + 2] = o2;
+                if (STATS) {
+                    const uint64_t kk = 3ull * ((uint64_t)tri_base + t);
+                    ws.cs_idx += mix64(((kk) << 32) | o0) + mix64(((kk + 1) << 32) | o1) + mix64(((kk + 2) << 32) | o2);
+                    ws.degen += (a0 == a1 || a1 == a2 || a0 == a2) ? 1u : 0u;
+                }
+            }
+        }
+        if (STATS) {
+            e2 = __reduce_or_sync(kFull, e2);
+            if (lane == 0) {
+                ws.tris += Tp;
+                ws.verts += V;
+                if (e2) {
+                    atomicOr(&P.stats->error_bits, e2);
+                    atomicMin(&P.stats->first_bad_meshlet, m);
+                    atomicAdd(&P.stats->num_bad, 1u);
+                }
+            }
+        }
+
+        // ---------------- a7/a8: attributes
+        const bool want_f = P.fout != nullptr, want_q = P.qout != nullptr;
+        if ((want_f || want_q) && (uint32_t)lane < 2u * P.n)
+            consts[lane] = __ldg(P.objtab + (size_t)object * 2u * P.n + lane);   // Δ[0..n), g[0..n)
+        __syncwarp();
+        // a6: indices out
+        warp_store_words(idst, ist, 3u * Tp, lane);
+
+        if (want_f || want_q) {
+            const uint32_t vpos = vtx_base - P.base_vtx;
+            float* fdst = want_f ? P.fout + (size_t)NOUT_RT * vpos : nullptr;
+            const uint32_t fphase = want_f ? ((uint32_t)(reinterpret_cast<uintptr_t>(fdst) >> 2) & 3u) : 0u;
+            uint32_t* vst = vtx_stage + fphase;
+            for (uint32_t v = lane; v < V; v += 32) {
+                // sequential little-endian bit reader over the vertex record (FORMAT.md §1.4)
+                const uint32_t bit0 = v * P.S;
+                const uint32_t* wp = AT + (bit0 >> 5);
+                uint64_t acc = (uint64_t)(wp[0] >> (bit0 & 31u));
+                uint32_t avail = 32u - (bit0 & 31u);
+                ++wp;
+                auto next_code = [&](uint32_t b) -> uint32_t {
+                    if (avail < b) { acc |= (uint64_t)(*wp++) << avail; avail += 32u; }
+                    const uint32_t code = (uint32_t)acc & ((1u << b) - 1u);
+                    acc >>= b;
+                    avail -= b;
+                    return code;
+                };
+                if constexpr (NCH > 0) {
+                    uint32_t qv[NCH];
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) qv[c] = R[4 + c] + next_code(P.bits[c]);   // q = L_c + code
+                    if (want_q) {
+                        uint32_t* qd = P.qout + (size_t)NCH * (vpos + v);
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) {
+                            qd[c] = qv[c];
+                            if (STATS) ws.cs_q += mix64((((uint64_t)NCH * (vtx_base + v) + c) << 32) | qv[c]);
+                        }
+                    }
+                    if (want_f) {
+                        float outv[NOUT];
+                        int o = 0;
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) {
+                            const float x = __fmaf_rn(__uint2float_rn(qv[c]), consts[c], consts[NCH + c]);
+                            if (c == OCT0) {
+                                const float y = __fmaf_rn(__uint2float_rn(qv[c + 1]), consts[c + 1], consts[NCH + c + 1]);
+                                oct_decode(x, y, outv[o], outv[o + 1], outv[o + 2]);
+                                o += 3;
+                            } else if (c != OCT0 + 1 || OCT0 < 0) {
+                                outv[o++] = x;
+                            }
+                        }
+                        if (STATS) {
+#pragma unroll
+                            for (int k2 = 0; k2 < NOUT; ++k2)
+                                ws.cs_f += mix64((((uint64_t)NOUT * (vtx_base + v) + k2) << 32) | __float_as_uint(outv[k2]));
+                        }
+                        if constexpr (NOUT % 4 == 0) {
+                            uint32_t* d = reinterpret_cast<uint32_t*>(fdst) + (size_t)NOUT * v;
+#pragma unroll
+                            for (int k2 = 0; k2 < NOUT; k2 += 4)
+                                st_v4(d + k2, make_uint4(__float_as_uint(outv[k2]), __float_as_uint(outv[k2 + 1]),
+                                                         __float_as_uint(outv[k2 + 2]), __float_as_uint(outv[k2 + 3])));
+                        } else {
+#pragma unroll
+                            for (int k2 = 0; k2 < NOUT; ++k2) vst[NOUT * v + k2] = __float_as_uint(outv[k2]);
+                        }
+                    }
+                } else {
+                    // generic layout: runtime channel loop, outputs through the smem stage
+                    uint32_t* qd = want_q ? P.qout + (size_t)P.n * (vpos + v) : nullptr;
+                    float xprev = 0.0f;
+                    for (uint32_t c = 0; c < P.n; ++c) {
+                        const uint32_t q = R[4 + c] + next_code(P.bits[c]);
+                        if (want_q) {
+                            qd[c] = q;
+                            if (STATS) ws.cs_q += mix64((((uint64_t)P.n * (vtx_base + v) + c) << 32) | q);
+                        }
+                        if (!want_f) continue;
+                        const float x = __fmaf_rn(__uint2float_rn(q), consts[c], consts[P.n + c]);
+                        const uint32_t col = P.col[c];
+                        if (P.oct[c]) { xprev = x; continue; }                 // first of an oct pair
+                        if (c > 0 && P.oct[c - 1]) {
+                            float ox, oy, oz;
+                            oct_decode(xprev, x, ox, oy, oz);
+                            const uint32_t cc = P.col[c - 1];
+                            vst[P.n_out * v + cc] = __float_as_uint(ox);
+                            vst[P.n_out * v + cc + 1] = __float_as_uint(oy);
+                            vst[P.n_out * v + cc + 2] = __float_as_uint(oz);
+                            if (STATS) {
+                                const uint64_t kb = (uint64_t)P.n_out * (vtx_base + v) + cc;
+                                ws.cs_f += mix64((kb << 32) | __float_as_uint(ox)) + mix64(((kb + 1) << 32) | __float_as_uint(oy)) +
+                                           mix64(((kb + 2) << 32) | __float_as_uint(oz));
+                            }
+                        } else {
+                            vst[P.n_out * v + col] = __float_as_uint(x);
+                            if (STATS) ws.cs_f += mix64((((uint64_t)P.n_out * (vtx_base + v) + col) << 32) | __float_as_uint(x));
+                        }
+                    }
+                }
+            }
+            if (want_f && !(NCH > 0 && NOUT % 4 == 0)) {
+                __syncwarp();
+                warp_store_words(reinterpret_cast<uint32_t*>(fdst), vst, NOUT_RT * V, lane);
+            }
+        }
+        __syncwarp();
+    }
+
+    if (STATS) {
+        // a10: warp reduction, one atomic per counter per warp
+        for (int d = 16; d > 0; d >>= 1) {
+            ws.cs_idx += __shfl_down_sync(kFull, ws.cs_idx, d);
+            ws.cs_f += __shfl_down_sync(kFull, ws.cs_f, d);
+            ws.cs_q += __shfl_down_sync(kFull, ws.cs_q, d);
+            ws.degen += __shfl_down_sync(kFull, ws.degen, d);
+            ws.multi += __shfl_down_sync(kFull, ws.multi, d);
+            ws.max_lb = max(ws.max_lb, __shfl_down_sync(kFull, ws.max_lb, d));
+        }
+        if (lane == 0) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->checksum_indices), ws.cs_idx);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->checksum_vertices), ws.cs_f);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->checksum_quantized), ws.cs_q);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->triangles), ws.tris);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->degenerate), ws.degen);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->vertices), ws.verts);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->multiword_lookbacks), ws.multi);
+            atomicMax(&P.stats->max_lookback, ws.max_lb);
+        }
+    }
+}
+
+__global__ void stats_reset_kernel(mc_stats* s) {
+    if (threadIdx.x == 0) {
+        s->checksum_indices = s->checksum_vertices = s->checksum_quantized = 0;
+        s->triangles = s->degenerate = s->vertices = s->multiword_lookbacks = 0;
+        s->max_lookback = 0;
+        s->error_bits = 0;
+        s->first_bad_meshlet = 0xFFFFFFFFu;
+        s->num_bad = 0;
+    }
+}
+
+// ------------------------------------------------------------------ host launch
+mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t& smem) {
+    if (!a || !a->layout || !a->d_blob || !a->d_indices) return MC_ERR_ARG;
+    const mc_layout& L = *a->layout;
+    if ((uint64_t)a->first + a->count > L.num_meshlets) return MC_ERR_ARG;
+    if (reinterpret_cast<uintptr_t>(a->d_blob) & 15u) return MC_ERR_ARG;
+    if ((reinterpret_cast<uintptr_t>(a->d_indices) & 3u) || (reinterpret_cast<uintptr_t>(a->d_vertices) & 15u) ||
+        (reinterpret_cast<uintptr_t>(a->d_quantized) & 3u))
+        return MC_ERR_ARG;
+    if (L.n < 1 || L.n > 16 || L.max_record_bytes == 0 || (L.max_record_bytes & 15u)) return MC_ERR_FORMAT;
+    const uint8_t* blob = static_cast<const uint8_t*>(a->d_blob);
+    P.rec = blob + L.off_rec;
+    P.dir = reinterpret_cast<const uint32_t*>(blob + L.off_dir);
+    P.objtab = reinterpret_cast<const float*>(blob + L.off_obj);
+    P.rec_section_bytes = L.total_bytes - L.off_rec;
+    P.first = a->first;
+    P.end = a->first + a->count;
+    P.O = L.num_objects;
+    P.vmax = L.v_max;
+    P.tmax = L.t_max;
+    P.n = L.n;
+    P.n_out = L.n_out;
+    P.S = L.S;
+    P.max_rec = L.max_record_bytes;
+    P.base_vtx = L.base_vtx;
+    P.base_tri = L.base_tri;
+    P.total_v = L.total_v;
+    P.total_tp = L.total_tp;
+    P.index_sub = (a->flags & MC_DECODE_BLOB_LOCAL_INDICES) ? L.base_vtx : 0u;
+    P.hdr_words = ((16u + 4u * L.n + 15u) & ~15u) / 4u;
+    P.buf_words = L.max_record_bytes / 4u + 4u;
+    P.idx_stage_words = (3u * L.t_max + 8u + 3u) & ~3u;
+    P.vtx_stage_words = a->d_vertices ? ((L.v_max * L.n_out + 8u + 3u) & ~3u) : 0u;
+    P.idx = a->d_indices;
+    P.fout = a->d_vertices;
+    P.qout = a->d_quantized;
+    P.stats = st;
+    uint32_t off = 0, col = 0;
+    for (uint32_t c = 0; c < 16; ++c) { P.bits[c] = 0; P.bitoff[c] = 0; P.col[c] = 0; P.oct[c] = 0; }
+    for (uint32_t c = 0; c < L.n; ++c) {
+        P.bits[c] = L.bits[c];
+        P.bitoff[c] = (uint8_t)off;
+        off += L.bits[c];
+        P.col[c] = (uint8_t)col;
+        if (L.semantic[c] == MC_SEM_NORMAL_OCT) {
+            P.oct[c] = 1;
+            P.bits[c + 1] = L.bits[c + 1];
+            P.bitoff[c + 1] = (uint8_t)off;
+            off += L.bits[c + 1];
+            P.col[c + 1] = (uint8_t)(col + 1);
+            col += 3;
+            ++c;
+        } else {
+            col += 1;
+        }
+    }
+    const uint32_t warp_words = 2 * P.buf_words + P.idx_stage_words + P.vtx_stage_words + kMiscWords;
+    smem = (size_t)warp_words * 4u * kWarpsPerCta + 128;
+    return MC_OK;
+}
+
+template <int CODEC, bool STATS, int NCH, int OCT0>
+mc_status launch_t(const Params& P, size_t smem, cudaStream_t s) {
+    auto kern = mc_decode_kernel<CODEC, STATS, NCH, OCT0>;
+    static std::mutex mu;
+    static size_t configured = 0;
+    static int sms = 0;
+    static int blocks_per_sm_cache[64] = {0};
+    {
+        std::lock_guard<std::mutex> g(mu);
+        if (smem > configured) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+                return MC_ERR_CUDA;
+            configured = smem;
+        }
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+    }
+    const size_t bucket = std::min<size_t>(63, smem / 4096);
+    int bps = blocks_per_sm_cache[bucket];
+    if (!bps) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kThreads, smem) != cudaSuccess) return MC_ERR_CUDA;
+        if (bps < 1) return MC_ERR_LIMITS;
+        blocks_per_sm_cache[bucket] = bps;
+    }
+    const uint32_t count = P.end - P.first;
+    uint64_t want = (count + kWarpsPerCta - 1) / kWarpsPerCta;
+    uint64_t cap = (uint64_t)sms * bps;
+    unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
+    kern<<<grid, kThreads, smem, s>>>(P);
+    return cudaGetLastError() == cudaSuccess ? MC_OK : MC_ERR_CUDA;
+}
+
+template <int CODEC, bool STATS>
+mc_status dispatch_layout(int lay, const Params& P, size_t smem, cudaStream_t s) {
+    switch (lay) {
+        case 1: return launch_t<CODEC, STATS, 8, -1>(P, smem, s);
+        case 2: return launch_t<CODEC, STATS, 7, 3>(P, smem, s);
+        case 3: return launch_t<CODEC, STATS, 3, -1>(P, smem, s);
+        default: return launch_t<CODEC, STATS, 0, -1>(P, smem, s);
+    }
+}
+
+mc_status dispatch_codec(uint32_t codec, bool stats, int lay, const Params& P, size_t smem, cudaStream_t s) {
+    if (codec == MC_CODEC_GTS)
+        return stats ? dispatch_layout<MC_CODEC_GTS, true>(lay, P, smem, s) : dispatch_layout<MC_CODEC_GTS, false>(lay, P, smem, s);
+    return stats ? dispatch_layout<MC_CODEC_GTS_REUSE, true>(lay, P, smem, s)
+                 : dispatch_layout<MC_CODEC_GTS_REUSE, false>(lay, P, smem, s);
+}
+
+mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s) {
+    Params P;
+    size_t smem = 0;
+    mc_status rc = build_params(a, st, P, smem);
+    if (rc != MC_OK) return rc;
+    if (a->count == 0) return MC_OK;
+    if (smem > 227u * 1024u) return MC_ERR_LIMITS;
+    // compile-time layouts for the BASELINE configs, generic kernel otherwise
+    const mc_layout& L = *a->layout;
+    int lay = 0;
+    int oct0 = -1;
+    for (uint32_t c = 0; c < L.n; ++c)
+        if (L.semantic[c] == MC_SEM_NORMAL_OCT) { oct0 = (int)c; break; }
+    uint32_t noct = L.n_out - L.n;
+    if (L.n == 8 && noct == 0) lay = 1;                   // pos3 + nrm3 + uv2
+    else if (L.n == 7 && noct == 1 && oct0 == 3) lay = 2; // pos3 + oct2 + uv2 (cfg3/cfg4)
+    else if (L.n == 3 && noct == 0) lay = 3;              // positions only (cfg2)
+    return dispatch_codec(L.codec, st != nullptr, lay, P, smem, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+mc_status mc_decode_meshlets(const mc_decode_args* args, void* stream) {
+    return launch(args, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+mc_status mc_decode_stats(const mc_decode_args* args, mc_stats* d_stats, void* stream) {
+    if (!d_stats) return MC_ERR_ARG;
+    return launch(args, d_stats, static_cast<cudaStream_t>(stream));
+}
+
+mc_status mc_stats_reset(mc_stats* d_stats, void* stream) {
+    if (!d_stats) return MC_ERR_ARG;
+    stats_reset_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(d_stats);
+    return cudaGetLastError() == cudaSuccess ? MC_OK : MC_ERR_CUDA;
+}
+
+mc_status mc_decode_host(const mc_host_decode_args* h, void* stream) {
+    if (!h || !h->layout || !h->h_blob || !h->d_blob || !h->h_indices || !h->d_indices) return MC_ERR_ARG;
+    if ((h->h_vertices == nullptr) != (h->d_vertices == nullptr)) return MC_ERR_ARG;
+    if ((h->h_quantized == nullptr) != (h->d_quantized == nullptr)) return MC_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const mc_layout& L = *h->layout;
+    if (cudaMemcpyAsync(h->d_blob, h->h_blob, L.total_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return MC_ERR_CUDA;
+    mc_decode_args a;
+    a.layout = h->layout;
+    a.d_blob = h->d_blob;
+    a.first = 0;
+    a.count = L.num_meshlets;
+    a.d_indices = h->d_indices;
+    a.d_vertices = h->d_vertices;
+    a.d_quantized = h->d_quantized;
+    a.flags = h->flags;
+    mc_status rc = launch(&a, nullptr, s);
+    if (rc != MC_OK) return rc;
+    if (cudaMemcpyAsync(h->h_indices, h->d_indices, 12ull * L.total_tp, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return MC_ERR_CUDA;
+    if (h->h_vertices &&
+        cudaMemcpyAsync(h->h_vertices, h->d_vertices, 4ull * L.n_out * L.total_v, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return MC_ERR_CUDA;
+    if (h->h_quantized &&
+        cudaMemcpyAsync(h->h_quantized, h->d_quantized, 4ull * L.n * L.total_v, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return MC_ERR_CUDA;
+    return MC_OK;
+}
+
+}  // extern "C"
