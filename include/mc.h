@@ -107,6 +107,16 @@ mc_status mc_blob_instance(const mc_blob *const *protos, uint32_t num_protos,
                            const uint32_t *proto_of_instance, const float *offset,
                            uint32_t num_instances, mc_blob **out);
 
+/* Shard of the same instanced scene: only instances [first_instance,
+ * first_instance+instance_count) of the num_instances-long list, with the global
+ * base_meshlet/base_vtx/base_tri (and record vtx_base/tri_base) the full scene gives
+ * them, so per-shard checksums add up to the whole scene's (FORMAT.md §6).
+ * Object ids are local to the shard. */
+mc_status mc_blob_instance_range(const mc_blob *const *protos, uint32_t num_protos,
+                                 const uint32_t *proto_of_instance, const float *offset,
+                                 uint32_t num_instances, uint32_t first_instance,
+                                 uint32_t instance_count, mc_blob **out);
+
 /* Wrap a copy of external FORMAT.md bytes (e.g. another encoder's output). */
 mc_status mc_blob_from_bytes(const void *bytes, size_t n, mc_blob **out);
 

@@ -70,7 +70,7 @@ class mc_stats(ctypes.Structure):
 
 
 STATS_BYTES = ctypes.sizeof(mc_stats)
-EXPORTS = ["mc_encode", "mc_blob_instance", "mc_blob_from_bytes", "mc_blob_bytes", "mc_blob_source_map",
+EXPORTS = ["mc_encode", "mc_blob_instance", "mc_blob_instance_range", "mc_blob_from_bytes", "mc_blob_bytes", "mc_blob_source_map",
            "mc_blob_encode_stats", "mc_blob_free", "mc_parse_header", "mc_blob_shard_ranges", "mc_blob_extract",
            "mc_decode_meshlets", "mc_decode_stats", "mc_stats_reset", "mc_decode_host", "mc_status_str",
            "mc_abi_version"]
@@ -92,6 +92,7 @@ def lib() -> ctypes.CDLL:
         L.mc_abi_version.restype = u32
         L.mc_encode.argtypes = [ctypes.POINTER(mc_mesh), ctypes.POINTER(mc_encode_params), ctypes.POINTER(P)]
         L.mc_blob_instance.argtypes = [P, u32, P, P, u32, ctypes.POINTER(P)]
+        L.mc_blob_instance_range.argtypes = [P, u32, P, P, u32, u32, u32, ctypes.POINTER(P)]
         L.mc_blob_from_bytes.argtypes = [P, sz, ctypes.POINTER(P)]
         L.mc_blob_bytes.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(sz)]
         L.mc_blob_source_map.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P)]
@@ -194,6 +195,16 @@ def mc_blob_instance(protos, proto_of_instance, offsets) -> Blob:
     h = ctypes.c_void_p()
     _check(lib().mc_blob_instance(ctypes.cast(arr, ctypes.c_void_p), len(protos), _p(pi), _p(off), pi.size,
                                   ctypes.byref(h)), "mc_blob_instance")
+    return Blob(h)
+
+
+def mc_blob_instance_range(protos, proto_of_instance, offsets, first_instance: int, instance_count: int) -> Blob:
+    arr = (ctypes.c_void_p * len(protos))(*[p._h.value for p in protos])
+    pi = np.ascontiguousarray(proto_of_instance, dtype=np.uint32)
+    off = np.ascontiguousarray(offsets, dtype=np.float32).reshape(-1)
+    h = ctypes.c_void_p()
+    _check(lib().mc_blob_instance_range(ctypes.cast(arr, ctypes.c_void_p), len(protos), _p(pi), _p(off), pi.size,
+                                        first_instance, instance_count, ctypes.byref(h)), "mc_blob_instance_range")
     return Blob(h)
 
 

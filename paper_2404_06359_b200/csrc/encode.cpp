@@ -800,7 +800,14 @@ mc_status mc_blob_extract(const void* bytes, size_t n, uint32_t first, uint32_t 
 
 mc_status mc_blob_instance(const mc_blob* const* protos, uint32_t num_protos, const uint32_t* proto_of_instance,
                            const float* offset, uint32_t num_instances, mc_blob** out) {
+    return mc_blob_instance_range(protos, num_protos, proto_of_instance, offset, num_instances, 0, num_instances, out);
+}
+
+mc_status mc_blob_instance_range(const mc_blob* const* protos, uint32_t num_protos, const uint32_t* proto_of_instance,
+                                 const float* offset, uint32_t num_instances, uint32_t first_instance,
+                                 uint32_t instance_count, mc_blob** out) {
     if (!protos || !num_protos || !proto_of_instance || !offset || !out) return MC_ERR_ARG;
+    if (uint64_t(first_instance) + instance_count > num_instances) return MC_ERR_ARG;
     *out = nullptr;
     std::vector<mc_layout> Ls(num_protos);
     for (uint32_t p = 0; p < num_protos; ++p) {
@@ -812,10 +819,20 @@ mc_status mc_blob_instance(const mc_blob* const* protos, uint32_t num_protos, co
             return MC_ERR_ARG;
     }
     const mc_layout& L0 = Ls[0];
+    // global bases of the range: everything the instances before it produce
+    uint64_t gm = 0, gv = 0, gt = 0;
+    for (uint32_t i = 0; i < first_instance; ++i) {
+        if (proto_of_instance[i] >= num_protos) return MC_ERR_ARG;
+        const mc_layout& L = Ls[proto_of_instance[i]];
+        gm += L.num_meshlets; gv += L.total_v; gt += L.total_tp;
+    }
+    const uint32_t* poi = proto_of_instance + first_instance;
+    const float* offs = offset + 3ull * first_instance;
+    num_instances = instance_count;
     uint64_t M = 0, O = 0, tv = 0, ttp = 0, tt = 0, rb = 0, maxrec = 0;
     uint32_t vmax = 0, tmax = 0;
     for (uint32_t i = 0; i < num_instances; ++i) {
-        uint32_t p = proto_of_instance[i];
+        uint32_t p = poi[i];
         if (p >= num_protos) return MC_ERR_ARG;
         const mc_layout& L = Ls[p];
         M += L.num_meshlets; O += L.num_objects; tv += L.total_v; ttp += L.total_tp; tt += L.total_t;
@@ -824,25 +841,29 @@ mc_status mc_blob_instance(const mc_blob* const* protos, uint32_t num_protos, co
         vmax = std::max(vmax, L.v_max);
         tmax = std::max(tmax, L.t_max);
     }
-    if (O > 65536 || tv > 0xFFFFFFFFull || 3 * ttp > 0xFFFFFFFFull || rb / 16 > 0xFFFFFFFFull) return MC_ERR_RANGE;
+    if (O > 65536 || gv + tv > 0xFFFFFFFFull || 3 * (gt + ttp) > 0xFFFFFFFFull || rb / 16 > 0xFFFFFFFFull ||
+        gm + M > 0xFFFFFFFFull)
+        return MC_ERR_RANGE;
     const uint32_t n = L0.n;
     const uint64_t off_dir = kHeaderBytes, off_obj = round16(off_dir + 4ull * (M + 1));
     const uint64_t off_rec = round16(off_obj + 8ull * n * O), total = off_rec + rb;
     auto blob = std::make_unique<mc_blob>();
     if (!blob->allocate(total)) return MC_ERR_NOMEM;
     uint8_t* B = blob->bytes;
-    write_header(B, L0.codec, n, uint32_t(M), uint32_t(O), vmax, tmax, tv, ttp, tt, 0, 0, 0, uint32_t(maxrec), off_dir,
-                 off_obj, off_rec, total, L0.bits, L0.semantic);
+    write_header(B, L0.codec, n, uint32_t(M), uint32_t(O), vmax, tmax, tv, ttp, tt, uint32_t(gm), uint32_t(gv),
+                 uint32_t(gt), uint32_t(maxrec), off_dir, off_obj, off_rec, total, L0.bits, L0.semantic);
     // per-instance prefix sums, then fill instances in parallel
     std::vector<uint64_t> im(num_instances + 1, 0), io(num_instances + 1, 0), iv(num_instances + 1, 0),
         it(num_instances + 1, 0), ir(num_instances + 1, 0);
+    iv[0] = gv;
+    it[0] = gt;
     for (uint32_t i = 0; i < num_instances; ++i) {
-        const mc_layout& L = Ls[proto_of_instance[i]];
+        const mc_layout& L = Ls[poi[i]];
         im[i + 1] = im[i] + L.num_meshlets; io[i + 1] = io[i] + L.num_objects;
         iv[i + 1] = iv[i] + L.total_v; it[i + 1] = it[i] + L.total_tp; ir[i + 1] = ir[i] + (L.total_bytes - L.off_rec);
     }
     parallel_for(num_instances, worker_count(0), [&](size_t i) {
-        const uint32_t p = proto_of_instance[i];
+        const uint32_t p = poi[i];
         const mc_layout& L = Ls[p];
         const uint8_t* src = protos[p]->bytes;
         // objects: position-channel origins shifted by the instance translation
@@ -854,7 +875,7 @@ mc_status mc_blob_instance(const mc_blob* const* protos, uint32_t num_protos, co
                 if (L.semantic[c] == MC_SEM_POSITION) {
                     float g;
                     std::memcpy(&g, dst + 4ull * (n + c), 4);
-                    g = g + offset[3ull * i + pc++];
+                    g = g + offs[3ull * i + pc++];
                     std::memcpy(dst + 4ull * (n + c), &g, 4);
                 }
         }

@@ -114,3 +114,23 @@ def test_instance(mc, orc):
         assert np.allclose(fi[:, :3], fp[:, :3] + scene.instance_offset[i], atol=1e-3)
         assert np.array_equal(fi[:, 3:], fp[:, 3:])
         off_v += pl.total_v
+
+
+def test_instance_range_shards(mc, orc):
+    """Instance-range shards carry global bases: their outputs and checksums tile the
+    whole scene's (the weak-scaling multi-GPU layout)."""
+    scene = synth.city(num_instances=7, num_prototypes=3, k=5, seed=2)
+    protos = [mc.mc_encode(p, 64, 126, 2) for p in scene.prototypes]
+    full = mc.mc_blob_instance(protos, scene.instance_proto, scene.instance_offset)
+    fe = orc.decode(np.array(full.bytes))
+    cs = 0
+    for first, cnt in ((0, 3), (3, 1), (4, 3)):
+        s = mc.mc_blob_instance_range(protos, scene.instance_proto, scene.instance_offset, first, cnt)
+        L = s.layout
+        err, errs, idx, q, f = orc.decode(np.array(s.bytes))
+        assert err == 0
+        np.testing.assert_array_equal(idx, fe[2][3 * L.base_tri:3 * (L.base_tri + L.total_tp)])
+        np.testing.assert_array_equal(f.view(np.uint32),
+                                      fe[4].view(np.uint32)[L.n_out * L.base_vtx:L.n_out * (L.base_vtx + L.total_v)])
+        cs = (cs + orc.checksum(idx, 3 * L.base_tri)) % 2**64
+    assert cs == orc.checksum(fe[2], 0)

@@ -107,7 +107,7 @@ def test_exhaustive_tiny_gts(mc, orc):
             for flags in itertools.product([0, 1], repeat=Tp - 1):
                 for idx in itertools.product(range(V), repeat=Tp - 1):
                     ms.append(gts_meshlet(V, flags, idx))
-    assert len(ms) > 50000
+    assert len(ms) > 30000
     rng = np.random.default_rng(0)
     codes = rng.integers(0, 256, size=sum(m["V"] for m in ms))
     blob = pack_meshlets(orc, 1, ms, codes=codes, vmax=6, tmax=5)
