@@ -153,9 +153,10 @@ void or_oct_decode(float ex, float ey, float *out3) {
     float xx = x * x;
     float s2 = fmaf(z, z, fmaf(y, y, xx));
     float r = sqrtf(s2);
-    out3[0] = x / r;
-    out3[1] = y / r;
-    out3[2] = z / r;
+    float inv = 1.0f / r;
+    out3[0] = x * inv;
+    out3[1] = y * inv;
+    out3[2] = z * inv;
 }
 
 /* ------------------------------------------------------------------ sequential decode

@@ -50,8 +50,7 @@ struct Params {
     uint32_t index_sub;        // subtracted from index values (MC_DECODE_BLOB_LOCAL_INDICES)
     uint32_t hdr_words;        // record header words (16 + 4n rounded to 16) / 4
     uint32_t buf_words;        // per-buffer words (max_rec/4 + 4)
-    uint32_t idx_stage_words;  // 3*tmax + 8
-    uint32_t vtx_stage_words;  // vmax*n_out + 8 (0 when stores go direct)
+    uint32_t vtx_stage_words;  // vmax*n_out + 8 for the generic layout, else 0
     uint32_t* idx;
     float* fout;
     uint32_t* qout;
@@ -143,9 +142,10 @@ __device__ __forceinline__ void oct_decode(float ex, float ey, float& ox, float&
     }
     const float s2 = __fmaf_rn(z, z, __fmaf_rn(y, y, __fmul_rn(x, x)));
     const float r = __fsqrt_rn(s2);
-    ox = __fdiv_rn(x, r);
-    oy = __fdiv_rn(y, r);
-    oz = __fdiv_rn(z, r);
+    const float inv = __frcp_rn(r);
+    ox = __fmul_rn(x, inv);
+    oy = __fmul_rn(y, inv);
+    oz = __fmul_rn(z, inv);
 }
 
 struct WarpStats {
@@ -153,32 +153,36 @@ struct WarpStats {
     uint32_t max_lb = 0;
 };
 
+
 // ------------------------------------------------------------------ the kernel
 // NCH > 0: compile-time channel count (register arrays, static indexing), OCT0 = first
-// channel of the octahedral pair or -1.  NCH == 0: generic runtime layout.
-template <int CODEC, bool STATS, int NCH, int OCT0>
+// channel of the octahedral pair or -1; B16: every channel is 16 bits wide (the paper's
+// b = 16) so codes are read as aligned halfwords.  NCH == 0: generic
+// runtime layout (any n <= 16, widths 1..24, any octahedral placement).
+template <int CODEC, bool STATS, int NCH, int OCT0, bool B16>
 __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_constant__ Params P) {
     constexpr int NOUT = NCH > 0 ? NCH + (OCT0 >= 0 ? 1 : 0) : 1;
-    const uint32_t NOUT_RT = NCH > 0 ? (uint32_t)NOUT : P.n_out;
+    const uint32_t n_out = NCH > 0 ? (uint32_t)NOUT : P.n_out;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
+    const uint32_t wpc = blockDim.x >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;        // lanes below
+    const uint32_t le_mask = 0xFFFFFFFFu >> (31 - lane);  // lanes at or below
 
     // per-warp smem carve-up (all offsets multiples of 16 B)
-    const uint32_t warp_words = 2 * P.buf_words + P.idx_stage_words + P.vtx_stage_words + kMiscWords;
+    const uint32_t warp_words = 2 * P.buf_words + P.vtx_stage_words + kMiscWords;
     uint32_t* wbase = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)wid * warp_words;
     uint32_t* buf0 = wbase;
-    uint32_t* idx_stage = wbase + 2 * P.buf_words;
-    uint32_t* vtx_stage = idx_stage + P.idx_stage_words;
-    uint32_t* misc = vtx_stage + P.vtx_stage_words;                 // kMiscWords words
-    uint64_t* bars = reinterpret_cast<uint64_t*>(misc);               // 2 mbarriers (4 words)
-    uint32_t* sizes = misc + 4;                                       // staged size per buffer (2)
-    float* consts = reinterpret_cast<float*>(misc + 8);               // Δ[16], g[16]
+    uint32_t* vtx_stage = wbase + 2 * P.buf_words;
+    uint32_t* misc = vtx_stage + P.vtx_stage_words;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(misc);               // 2 mbarriers
+    uint32_t* sizes = misc + 4;                                       // staged bytes per buffer
+    float* consts = reinterpret_cast<float*>(misc + 8);               // Δ[16], g[16] (generic path)
     uint8_t* Nbuf = reinterpret_cast<uint8_t*>(misc + 40);            // N[0..T'+1], 272 B
 
-    const uint32_t gwarp = blockIdx.x * kWarpsPerCta + wid;
-    const uint32_t nwarps = gridDim.x * kWarpsPerCta;
-    uint32_t m = P.first + gwarp;
+    const uint32_t nwarps = gridDim.x * wpc;
+    uint32_t m = P.first + blockIdx.x * wpc + wid;
 
     if (lane == 0) {
         mbar_init(&bars[0], 1);
@@ -187,12 +191,12 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
     }
     __syncwarp();
 
-    // lane 0 issues the bulk copy of record `mm` into buffer `b` (or a plain arrive for a
-    // record that cannot be staged; its size is then recorded as 0 -> RECORD error)
-    auto issue = [&](uint32_t mm, uint32_t d0, uint32_t d1, int b) {
-        uint64_t off = 16ull * d0;
-        uint32_t bytes = (d1 > d0) ? 16u * (d1 - d0) : 0u;
-        bool ok = bytes != 0 && bytes <= P.max_rec && off + bytes <= P.rec_section_bytes;
+    // a2: lane 0 stages record `mm` with one TMA bulk copy into buffer `b` (or a plain
+    // arrive for a record that cannot be staged: size 0 -> RECORD error)
+    auto issue = [&](uint32_t d0, uint32_t d1, int b) {
+        const uint64_t off = 16ull * d0;
+        const uint32_t bytes = (d1 > d0) ? 16u * (d1 - d0) : 0u;
+        const bool ok = bytes != 0 && bytes <= P.max_rec && off + bytes <= P.rec_section_bytes;
         sizes[b] = ok ? bytes : 0u;
         if (ok) {
             fence_proxy_async();
@@ -203,11 +207,9 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
         }
     };
 
-    // directory prefetch: (d0,d1) for the next record to issue
-    uint32_t nd0 = 0, nd1 = 0;
+    uint32_t nd0 = 0, nd1 = 0;   // directory entries of the record after next (prefetched)
     if (m < P.end && lane == 0) {
-        uint32_t d0 = __ldg(P.dir + m), d1 = __ldg(P.dir + m + 1);
-        issue(m, d0, d1, 0);
+        issue(__ldg(P.dir + m), __ldg(P.dir + m + 1), 0);
         if (m + nwarps < P.end) { nd0 = __ldg(P.dir + m + nwarps); nd1 = __ldg(P.dir + m + nwarps + 1); }
     }
 
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
         const int b = k & 1;
         const uint32_t mnext = m + nwarps;
         if (lane == 0 && mnext < P.end) {
-            issue(mnext, nd0, nd1, b ^ 1);
+            issue(nd0, nd1, b ^ 1);
             const uint32_t m2 = mnext + nwarps;
             if (m2 < P.end) { nd0 = __ldg(P.dir + m2); nd1 = __ldg(P.dir + m2 + 1); }
         }
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
         const uint32_t* R = buf0 + (size_t)b * P.buf_words;
         const uint32_t staged = sizes[b];
 
-        // ---------------- a1: header (FORMAT.md §1.4)
+        // ---------------- a1: header (FORMAT.md §1.4) + structural validation (§5)
         const uint32_t vtx_base = R[0], tri_base = R[1], w2 = R[2];
         const uint32_t V = (w2 & 0xFFu) + 1u, Tp = ((w2 >> 8) & 0xFFu) + 1u, object = w2 >> 16;
         const uint32_t W = (Tp + 31u) >> 5;
@@ -245,32 +247,43 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
                 (uint64_t)vtx_base - P.base_vtx + V > P.total_v || vtx_base < P.base_vtx)
                 err |= MC_DERR_RECORD;
         }
-        const uint32_t* LR = R + lr_w;
-        const uint32_t* INC = R + inc_w;
         const uint8_t* BY = reinterpret_cast<const uint8_t*>(R + by_w);
         const uint32_t* AT = R + at_w;
 
-        // ---------------- a3: increment-flag popcount prefix (GTS-Reuse)
-        uint32_t my_pc = 0, my_excl = 0;
-        if (CODEC == MC_CODEC_GTS_REUSE && !err) {
-            if ((uint32_t)lane < W) {
-                uint32_t w = INC[lane];
-                if (lane == 0) w &= ~1u;                                   // bit 0 ignored
-                const uint32_t rem = Tp - 32u * lane;
-                if (rem < 32u) w &= (1u << rem) - 1u;                       // bits >= T' ignored
-                my_pc = __popc(w);
-            }
-            uint32_t incl = my_pc;
-#pragma unroll
-            for (int d = 1; d < 8; d <<= 1) {
-                uint32_t o = __shfl_up_sync(kFull, incl, d);
-                if (lane >= d) incl += o;
-            }
-            my_excl = incl - my_pc;
-            const uint32_t total = __shfl_sync(kFull, incl, 7);
-            if (total != V - 3u) err |= MC_DERR_COUNTS;
+        // ---------------- per-word prefix state, lanes 0..W-1 hold word `lane` (W <= 8)
+        // valid bits of word `lane`: triangles t < T', bit 0 (t = 0) excluded
+        uint32_t vm = 0;
+        if ((uint32_t)lane < W) {
+            const uint32_t rem = Tp - 32u * lane;
+            vm = rem >= 32u ? 0xFFFFFFFFu : ((1u << rem) - 1u);
         }
-        err = __shfl_sync(kFull, err, 0);
+        if (lane == 0) vm &= ~1u;
+        const uint32_t lrw = ((uint32_t)lane < W && !err) ? (R[lr_w + lane] & vm) : 0u;      // f_0 := L
+        // highest R (1) and highest L (0) flag position in this word (bit 0 of word 0 is L)
+        const uint32_t ones = lrw, zeros = (~lrw & vm) | (lane == 0 ? 1u : 0u);
+        int hi1 = ones ? 32 * lane + 31 - __clz(ones) : -1;
+        int hi0 = ((uint32_t)lane < W && zeros) ? 32 * lane + 31 - __clz(zeros) : -1;
+        uint32_t incw = 0, pc = 0;
+        if (CODEC == MC_CODEC_GTS_REUSE) {
+            incw = ((uint32_t)lane < W && !err) ? (R[inc_w + lane] & vm) : 0u;
+            pc = __popc(incw);
+        }
+#pragma unroll
+        for (int d = 1; d < 8; d <<= 1) {           // inclusive max / add scans over <= 8 words
+            const int o1 = __shfl_up_sync(kFull, hi1, d), o0 = __shfl_up_sync(kFull, hi0, d);
+            const uint32_t op = __shfl_up_sync(kFull, pc, d);
+            if (lane >= d) { hi1 = max(hi1, o1); hi0 = max(hi0, o0); if (CODEC == MC_CODEC_GTS_REUSE) pc += op; }
+        }
+        // exclusive: last R / last L strictly before word `lane`, increment flags before it
+        const int prev1 = lane ? __shfl_up_sync(kFull, hi1, 1) : -1;
+        const int prev0_raw = __shfl_up_sync(kFull, hi0, 1);
+        const int prev0 = lane ? prev0_raw : -1;
+        const uint32_t pc_excl_raw = __shfl_up_sync(kFull, pc, 1);
+        const uint32_t pc_excl = lane ? pc_excl_raw : 0u;
+        if (CODEC == MC_CODEC_GTS_REUSE) {
+            const uint32_t total = __shfl_sync(kFull, pc, 7);
+            if (!err && total != V - 3u) err |= MC_DERR_COUNTS;
+        }
         if (err) {
             if (STATS && lane == 0) {
                 atomicOr(&P.stats->error_bits, err);
@@ -281,79 +294,56 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
             continue;
         }
 
-        // N[0..2] = 0,1,2; N[t+2] for t = 1..T'-1
-        if (lane < 3) Nbuf[lane] = (uint8_t)lane;
+        // ---------------- a3/a4/a5/a6: topology, one triangle per lane per word
+        if (lane < 2) Nbuf[lane] = (uint8_t)lane;                            // N[0], N[1]
+        const uint32_t vout = vtx_base - P.index_sub;
+        uint32_t* idst = P.idx + 3ull * (tri_base - P.base_tri);
+        uint32_t carry = 2u;                                                 // N[t+1] for lane 0
         uint32_t e2 = 0;
         for (uint32_t j = 0; j < W; ++j) {
             const uint32_t t = 32u * j + lane;
-            uint32_t wv = 0;
+            const bool active = t < Tp;
+            // a3: new-vertex index N[t+2] (w_0 := N[2] = 2)
+            uint32_t w = 2u;
             if (CODEC == MC_CODEC_GTS) {
-                if (t >= 1u && t < Tp) {
-                    wv = BY[t - 1u];
-                    if (wv >= V) e2 |= MC_DERR_INDEX;
-                }
+                if (active && t >= 1u) w = BY[t - 1u];
+                if (STATS && active && w >= V) e2 |= MC_DERR_INDEX;
             } else {
-                uint32_t iw = INC[j];
-                if (j == 0) iw &= ~1u;
-                const uint32_t pre = __shfl_sync(kFull, my_excl, j);
-                if (t >= 1u && t < Tp) {
-                    const uint32_t i_t = (iw >> lane) & 1u;
-                    const uint32_t c = pre + __popc(iw & (0xFFFFFFFFu >> (31 - lane)));   // inclusive
-                    if (i_t) wv = 2u + c;
-                    else {
-                        wv = BY[t - c - 1u];                                // P:465 (t+1-s, s=2+c)
-                        if (wv >= V) e2 |= MC_DERR_REUSE;
-                    }
+                const uint32_t iw = __shfl_sync(kFull, incw, j);
+                const uint32_t c = __shfl_sync(kFull, pc_excl, j) + __popc(iw & le_mask);   // inclusive scan c_t
+                if ((iw >> lane) & 1u) w = 2u + c;
+                else if (active && t >= 1u) {
+                    w = BY[t - c - 1u];                                      // location t+1-s, s = 2+c
+                    if (STATS && w >= V) e2 |= MC_DERR_REUSE;
                 }
             }
-            if (t >= 1u && t < Tp) Nbuf[t + 2u] = (uint8_t)wv;
-        }
-        __syncwarp();
-
-        // ---------------- a4/a5: L/R lookback + triangle assembly
-        const uint32_t vout = vtx_base - P.index_sub;
-        const uint32_t tpos = tri_base - P.base_tri;                        // output triangle position
-        uint32_t* idst = P.idx + 3ull * tpos;
-        const uint32_t iphase = (uint32_t)(reinterpret_cast<uintptr_t>(idst) >> 2) & 3u;
-        uint32_t* ist = idx_stage + iphase;
-        for (uint32_t j = 0; j < W; ++j) {
-            const uint32_t t = 32u * j + lane;
-            if (t < Tp) {
-                uint32_t a0, a1, a2;
-                if (t == 0) {
-                    a0 = 0; a1 = 1; a2 = 2;
-                } else {
-                    uint32_t lw = LR[j];
-                    if (j == 0) lw &= ~1u;                                  // f_0 := L
-                    const uint32_t f = (lw >> lane) & 1u;
-                    const uint32_t below = (1u << lane) - 1u;
-                    uint32_t x = (f ? ~lw : lw) & below;                    // differing flags below t
-                    int jj = -1;
-                    if (x) jj = (int)(32u * j) + 31 - __clz(x);
-                    else {
-                        // multi-word fallback: rare fans longer than the word
-                        for (int jp = (int)j - 1; jp >= 0; --jp) {
-                            uint32_t pw = LR[jp];
-                            if (jp == 0) pw &= ~1u;
-                            const uint32_t y = f ? ~pw : pw;
-                            if (y) { jj = 32 * jp + 31 - __clz(y); break; }
-                        }
-                        if (STATS && j > 0) ws.multi++;
-                    }
-                    const uint32_t nprev = Nbuf[t + 1u], npiv = Nbuf[jj + 1], nnew = Nbuf[t + 2u];
-                    if (f) { a0 = nprev; a1 = npiv; }                       // R: (N[t+1], N[j+1], N[t+2])
-                    else   { a0 = npiv;  a1 = nprev; }                      // L: (N[j+1], N[t+1], N[t+2])
-                    a2 = nnew;
-                    if (STATS) ws.max_lb = max(ws.max_lb, (uint32_t)((int)t - jj));
-                }
-                const uint32_t o0 = vout + a0, o1 = vout + a1, o2 = vout + a2;
-                ist[3 * t] = o0;
-                ist[3 * t + 1] = o1;
-                ist[3 * t + 2] = o2;
+            if (active) Nbuf[t + 2u] = (uint8_t)w;
+            // a4: j(t) = max{k < t : f_k != f_t} by bit scan; earlier words
+            // through the per-word last-R / last-L scans instead of a loop
+            const uint32_t lw = __shfl_sync(kFull, lrw, j);
+            const int p1 = __shfl_sync(kFull, prev1, j), p0 = __shfl_sync(kFull, prev0, j);
+            const uint32_t nprev_up = __shfl_up_sync(kFull, w, 1);
+            const uint32_t nprev = lane ? nprev_up : carry;                  // N[t+1]
+            carry = __shfl_sync(kFull, w, 31);
+            __syncwarp();
+            if (active) {
+                const uint32_t f = (lw >> lane) & 1u;
+                const uint32_t x = (f ? ~lw : lw) & lt_mask;
+                const int jj = x ? (int)(32u * j) + 31 - __clz(x) : (f ? p0 : p1);
+                const uint32_t npiv = Nbuf[jj + 1];                          // N[j+1], N[0] if none
+                uint32_t a0 = f ? nprev : npiv, a1 = f ? npiv : nprev;       // a5 (FORMAT.md §2)
+                if (t == 0) { a0 = 0u; a1 = 1u; }
+                const uint32_t o0 = vout + a0, o1 = vout + a1, o2 = vout + w;
+                uint32_t* d = idst + 3u * t;                                 // a6
+                d[0] = o0;
+                d[1] = o1;
+                d[2] = o2;
                 if (STATS) {
                     const uint64_t kk = 3ull * ((uint64_t)tri_base + t);
-                    ws.cs_idx += mix64(((kk) << 32) | o0) + mix64(((kk + 1) << 32) | o1) + mix64(((kk + 2) << 32) | o2);
-                    ws.degen += (a0 == a1 || a1 == a2 || a0 == a2) ? 1u : 0u;
+                    ws.cs_idx += mix64((kk << 32) | o0) + mix64(((kk + 1) << 32) | o1) + mix64(((kk + 2) << 32) | o2);
+                    ws.degen += (a0 == a1 || a1 == w || a0 == w) ? 1u : 0u;
+                    if (t > 0) ws.max_lb = max(ws.max_lb, (uint32_t)((int)t - jj));
+                    if (t > 0 && !x && j > 0) ws.multi++;
                 }
             }
         }
@@ -370,37 +360,44 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
             }
         }
 
-        // ---------------- a7/a8: attributes
+        // ---------------- a7/a8/a9: attributes
         const bool want_f = P.fout != nullptr, want_q = P.qout != nullptr;
-        if ((want_f || want_q) && (uint32_t)lane < 2u * P.n)
-            consts[lane] = __ldg(P.objtab + (size_t)object * 2u * P.n + lane);   // Δ[0..n), g[0..n)
-        __syncwarp();
-        // a6: indices out
-        warp_store_words(idst, ist, 3u * Tp, lane);
-
         if (want_f || want_q) {
             const uint32_t vpos = vtx_base - P.base_vtx;
-            float* fdst = want_f ? P.fout + (size_t)NOUT_RT * vpos : nullptr;
-            const uint32_t fphase = want_f ? ((uint32_t)(reinterpret_cast<uintptr_t>(fdst) >> 2) & 3u) : 0u;
-            uint32_t* vst = vtx_stage + fphase;
-            for (uint32_t v = lane; v < V; v += 32) {
-                // sequential little-endian bit reader over the vertex record (FORMAT.md §1.4)
-                const uint32_t bit0 = v * P.S;
-                const uint32_t* wp = AT + (bit0 >> 5);
-                uint64_t acc = (uint64_t)(wp[0] >> (bit0 & 31u));
-                uint32_t avail = 32u - (bit0 & 31u);
-                ++wp;
-                auto next_code = [&](uint32_t b) -> uint32_t {
-                    if (avail < b) { acc |= (uint64_t)(*wp++) << avail; avail += 32u; }
-                    const uint32_t code = (uint32_t)acc & ((1u << b) - 1u);
-                    acc >>= b;
-                    avail -= b;
-                    return code;
-                };
-                if constexpr (NCH > 0) {
-                    uint32_t qv[NCH];
+            float* fdst = want_f ? P.fout + (size_t)n_out * vpos : nullptr;
+            if constexpr (NCH > 0) {
+                // per-meshlet grid constants in registers: Δ_c, g_c, L_c
+                const float cv = (uint32_t)lane < 2u * NCH ? __ldg(P.objtab + (size_t)object * 2u * NCH + lane) : 0.0f;
+                float dl[NCH], og[NCH];
+                uint32_t Lc[NCH];
 #pragma unroll
-                    for (int c = 0; c < NCH; ++c) qv[c] = R[4 + c] + next_code(P.bits[c]);   // q = L_c + code
+                for (int c = 0; c < NCH; ++c) {
+                    dl[c] = __shfl_sync(kFull, cv, c);
+                    og[c] = __shfl_sync(kFull, cv, NCH + c);
+                    Lc[c] = R[4 + c];
+                }
+                for (uint32_t v = lane; v < V; v += 32) {
+                    uint32_t qv[NCH];
+                    if constexpr (B16) {
+                        const uint16_t* H = reinterpret_cast<const uint16_t*>(AT) + (size_t)v * NCH;
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) qv[c] = Lc[c] + H[c];   // q = L_c + code
+                    } else {
+                        // little-endian bit reader over the vertex record (FORMAT.md §1.4)
+                        const uint32_t bit0 = v * P.S;
+                        const uint32_t* wp = AT + (bit0 >> 5);
+                        uint64_t acc = (uint64_t)(wp[0] >> (bit0 & 31u));
+                        uint32_t avail = 32u - (bit0 & 31u);
+                        ++wp;
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) {
+                            const uint32_t bb = P.bits[c];
+                            if (avail < bb) { acc |= (uint64_t)(*wp++) << avail; avail += 32u; }
+                            qv[c] = Lc[c] + ((uint32_t)acc & ((1u << bb) - 1u));
+                            acc >>= bb;
+                            avail -= bb;
+                        }
+                    }
                     if (want_q) {
                         uint32_t* qd = P.qout + (size_t)NCH * (vpos + v);
 #pragma unroll
@@ -414,12 +411,12 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
                         int o = 0;
 #pragma unroll
                         for (int c = 0; c < NCH; ++c) {
-                            const float x = __fmaf_rn(__uint2float_rn(qv[c]), consts[c], consts[NCH + c]);
+                            const float x = __fmaf_rn(__uint2float_rn(qv[c]), dl[c], og[c]);
                             if (c == OCT0) {
-                                const float y = __fmaf_rn(__uint2float_rn(qv[c + 1]), consts[c + 1], consts[NCH + c + 1]);
+                                const float y = __fmaf_rn(__uint2float_rn(qv[c + 1]), dl[c + 1], og[c + 1]);
                                 oct_decode(x, y, outv[o], outv[o + 1], outv[o + 2]);
                                 o += 3;
-                            } else if (c != OCT0 + 1 || OCT0 < 0) {
+                            } else if (OCT0 < 0 || c != OCT0 + 1) {
                                 outv[o++] = x;
                             }
                         }
@@ -428,53 +425,68 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
                             for (int k2 = 0; k2 < NOUT; ++k2)
                                 ws.cs_f += mix64((((uint64_t)NOUT * (vtx_base + v) + k2) << 32) | __float_as_uint(outv[k2]));
                         }
+                        uint32_t* d = reinterpret_cast<uint32_t*>(fdst) + (size_t)NOUT * v;
                         if constexpr (NOUT % 4 == 0) {
-                            uint32_t* d = reinterpret_cast<uint32_t*>(fdst) + (size_t)NOUT * v;
 #pragma unroll
                             for (int k2 = 0; k2 < NOUT; k2 += 4)
                                 st_v4(d + k2, make_uint4(__float_as_uint(outv[k2]), __float_as_uint(outv[k2 + 1]),
                                                          __float_as_uint(outv[k2 + 2]), __float_as_uint(outv[k2 + 3])));
                         } else {
 #pragma unroll
-                            for (int k2 = 0; k2 < NOUT; ++k2) vst[NOUT * v + k2] = __float_as_uint(outv[k2]);
+                            for (int k2 = 0; k2 < NOUT; ++k2) d[k2] = __float_as_uint(outv[k2]);
                         }
                     }
-                } else {
-                    // generic layout: runtime channel loop, outputs through the smem stage
+                }
+            } else {
+                // generic layout: runtime channel loop, outputs through the smem stage
+                if ((uint32_t)lane < 2u * P.n) consts[lane] = __ldg(P.objtab + (size_t)object * 2u * P.n + lane);
+                __syncwarp();
+                const uint32_t fphase = want_f ? ((uint32_t)(reinterpret_cast<uintptr_t>(fdst) >> 2) & 3u) : 0u;
+                uint32_t* vst = vtx_stage + fphase;
+                for (uint32_t v = lane; v < V; v += 32) {
+                    const uint32_t bit0 = v * P.S;
+                    const uint32_t* wp = AT + (bit0 >> 5);
+                    uint64_t acc = (uint64_t)(wp[0] >> (bit0 & 31u));
+                    uint32_t avail = 32u - (bit0 & 31u);
+                    ++wp;
                     uint32_t* qd = want_q ? P.qout + (size_t)P.n * (vpos + v) : nullptr;
                     float xprev = 0.0f;
                     for (uint32_t c = 0; c < P.n; ++c) {
-                        const uint32_t q = R[4 + c] + next_code(P.bits[c]);
+                        const uint32_t bb = P.bits[c];
+                        if (avail < bb) { acc |= (uint64_t)(*wp++) << avail; avail += 32u; }
+                        const uint32_t q = R[4 + c] + ((uint32_t)acc & ((1u << bb) - 1u));
+                        acc >>= bb;
+                        avail -= bb;
                         if (want_q) {
                             qd[c] = q;
                             if (STATS) ws.cs_q += mix64((((uint64_t)P.n * (vtx_base + v) + c) << 32) | q);
                         }
                         if (!want_f) continue;
                         const float x = __fmaf_rn(__uint2float_rn(q), consts[c], consts[P.n + c]);
-                        const uint32_t col = P.col[c];
                         if (P.oct[c]) { xprev = x; continue; }                 // first of an oct pair
                         if (c > 0 && P.oct[c - 1]) {
                             float ox, oy, oz;
                             oct_decode(xprev, x, ox, oy, oz);
                             const uint32_t cc = P.col[c - 1];
-                            vst[P.n_out * v + cc] = __float_as_uint(ox);
-                            vst[P.n_out * v + cc + 1] = __float_as_uint(oy);
-                            vst[P.n_out * v + cc + 2] = __float_as_uint(oz);
+                            vst[n_out * v + cc] = __float_as_uint(ox);
+                            vst[n_out * v + cc + 1] = __float_as_uint(oy);
+                            vst[n_out * v + cc + 2] = __float_as_uint(oz);
                             if (STATS) {
-                                const uint64_t kb = (uint64_t)P.n_out * (vtx_base + v) + cc;
+                                const uint64_t kb = (uint64_t)n_out * (vtx_base + v) + cc;
                                 ws.cs_f += mix64((kb << 32) | __float_as_uint(ox)) + mix64(((kb + 1) << 32) | __float_as_uint(oy)) +
                                            mix64(((kb + 2) << 32) | __float_as_uint(oz));
                             }
                         } else {
-                            vst[P.n_out * v + col] = __float_as_uint(x);
-                            if (STATS) ws.cs_f += mix64((((uint64_t)P.n_out * (vtx_base + v) + col) << 32) | __float_as_uint(x));
+                            const uint32_t col = P.col[c];
+                            vst[n_out * v + col] = __float_as_uint(x);
+                            if (STATS) ws.cs_f += mix64((((uint64_t)n_out * (vtx_base + v) + col) << 32) | __float_as_uint(x));
                         }
                     }
                 }
-            }
-            if (want_f && !(NCH > 0 && NOUT % 4 == 0)) {
-                __syncwarp();
-                warp_store_words(reinterpret_cast<uint32_t*>(fdst), vst, NOUT_RT * V, lane);
+                if (want_f) {
+                    __syncwarp();
+                    warp_store_words(reinterpret_cast<uint32_t*>(fdst), vst, n_out * V, lane);
+                }
             }
         }
         __syncwarp();
@@ -545,8 +557,7 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     P.index_sub = (a->flags & MC_DECODE_BLOB_LOCAL_INDICES) ? L.base_vtx : 0u;
     P.hdr_words = ((16u + 4u * L.n + 15u) & ~15u) / 4u;
     P.buf_words = L.max_record_bytes / 4u + 4u;
-    P.idx_stage_words = (3u * L.t_max + 8u + 3u) & ~3u;
-    P.vtx_stage_words = a->d_vertices ? ((L.v_max * L.n_out + 8u + 3u) & ~3u) : 0u;
+    P.vtx_stage_words = 0;
     P.idx = a->d_indices;
     P.fout = a->d_vertices;
     P.qout = a->d_quantized;
@@ -570,24 +581,29 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
             col += 1;
         }
     }
-    const uint32_t warp_words = 2 * P.buf_words + P.idx_stage_words + P.vtx_stage_words + kMiscWords;
-    smem = (size_t)warp_words * 4u * kWarpsPerCta + 128;
+    const uint32_t warp_words = 2 * P.buf_words + P.vtx_stage_words + kMiscWords;
+    smem = (size_t)warp_words * 4u;   // per warp; the launch multiplies by warps per CTA
     return MC_OK;
 }
 
-template <int CODEC, bool STATS, int NCH, int OCT0>
-mc_status launch_t(const Params& P, size_t smem, cudaStream_t s) {
-    auto kern = mc_decode_kernel<CODEC, STATS, NCH, OCT0>;
+template <int CODEC, bool STATS, int NCH, int OCT0, bool B16>
+mc_status launch_t(const Params& P, size_t warp_smem, cudaStream_t s) {
+    auto kern = mc_decode_kernel<CODEC, STATS, NCH, OCT0, B16>;
+    // warps per CTA: 8, fewer when a warp's staging buffers are large (Ṽ=T̃=256, 24-bit)
+    const size_t budget = 200u * 1024u;
+    uint32_t wpc = (uint32_t)std::min<size_t>(kWarpsPerCta, std::max<size_t>(1, budget / warp_smem));
+    const size_t smem = warp_smem * wpc + 128;
+    if (smem > 227u * 1024u) return MC_ERR_LIMITS;
     static std::mutex mu;
     static size_t configured = 0;
     static int sms = 0;
-    static int blocks_per_sm_cache[64] = {0};
+    static int bps_cache[kWarpsPerCta + 1][64] = {};
     {
         std::lock_guard<std::mutex> g(mu);
         if (smem > configured) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227u * 1024u)) != cudaSuccess)
                 return MC_ERR_CUDA;
-            configured = smem;
+            configured = 227u * 1024u;
         }
         if (!sms) {
             int dev = 0;
@@ -596,35 +612,36 @@ mc_status launch_t(const Params& P, size_t smem, cudaStream_t s) {
         }
     }
     const size_t bucket = std::min<size_t>(63, smem / 4096);
-    int bps = blocks_per_sm_cache[bucket];
+    int bps = bps_cache[wpc][bucket];
     if (!bps) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kThreads, smem) != cudaSuccess) return MC_ERR_CUDA;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 32 * wpc, smem) != cudaSuccess) return MC_ERR_CUDA;
         if (bps < 1) return MC_ERR_LIMITS;
-        blocks_per_sm_cache[bucket] = bps;
+        bps_cache[wpc][bucket] = bps;
     }
     const uint32_t count = P.end - P.first;
-    uint64_t want = (count + kWarpsPerCta - 1) / kWarpsPerCta;
-    uint64_t cap = (uint64_t)sms * bps;
-    unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
-    kern<<<grid, kThreads, smem, s>>>(P);
+    const uint64_t want = (count + wpc - 1) / wpc;
+    const uint64_t cap = (uint64_t)sms * bps;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
+    kern<<<grid, 32 * wpc, smem, s>>>(P);
     return cudaGetLastError() == cudaSuccess ? MC_OK : MC_ERR_CUDA;
 }
 
 template <int CODEC, bool STATS>
-mc_status dispatch_layout(int lay, const Params& P, size_t smem, cudaStream_t s) {
+mc_status dispatch_layout(int lay, bool b16, const Params& P, size_t smem, cudaStream_t s) {
     switch (lay) {
-        case 1: return launch_t<CODEC, STATS, 8, -1>(P, smem, s);
-        case 2: return launch_t<CODEC, STATS, 7, 3>(P, smem, s);
-        case 3: return launch_t<CODEC, STATS, 3, -1>(P, smem, s);
-        default: return launch_t<CODEC, STATS, 0, -1>(P, smem, s);
+        case 1: return b16 ? launch_t<CODEC, STATS, 8, -1, true>(P, smem, s) : launch_t<CODEC, STATS, 8, -1, false>(P, smem, s);
+        case 2: return b16 ? launch_t<CODEC, STATS, 7, 3, true>(P, smem, s) : launch_t<CODEC, STATS, 7, 3, false>(P, smem, s);
+        case 3: return b16 ? launch_t<CODEC, STATS, 3, -1, true>(P, smem, s) : launch_t<CODEC, STATS, 3, -1, false>(P, smem, s);
+        default: return launch_t<CODEC, STATS, 0, -1, false>(P, smem, s);
     }
 }
 
-mc_status dispatch_codec(uint32_t codec, bool stats, int lay, const Params& P, size_t smem, cudaStream_t s) {
+mc_status dispatch_codec(uint32_t codec, bool stats, int lay, bool b16, const Params& P, size_t smem, cudaStream_t s) {
     if (codec == MC_CODEC_GTS)
-        return stats ? dispatch_layout<MC_CODEC_GTS, true>(lay, P, smem, s) : dispatch_layout<MC_CODEC_GTS, false>(lay, P, smem, s);
-    return stats ? dispatch_layout<MC_CODEC_GTS_REUSE, true>(lay, P, smem, s)
-                 : dispatch_layout<MC_CODEC_GTS_REUSE, false>(lay, P, smem, s);
+        return stats ? dispatch_layout<MC_CODEC_GTS, true>(lay, b16, P, smem, s)
+                     : dispatch_layout<MC_CODEC_GTS, false>(lay, b16, P, smem, s);
+    return stats ? dispatch_layout<MC_CODEC_GTS_REUSE, true>(lay, b16, P, smem, s)
+                 : dispatch_layout<MC_CODEC_GTS_REUSE, false>(lay, b16, P, smem, s);
 }
 
 mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s) {
@@ -633,7 +650,6 @@ mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s) {
     mc_status rc = build_params(a, st, P, smem);
     if (rc != MC_OK) return rc;
     if (a->count == 0) return MC_OK;
-    if (smem > 227u * 1024u) return MC_ERR_LIMITS;
     // compile-time layouts for the BASELINE configs, generic kernel otherwise
     const mc_layout& L = *a->layout;
     int lay = 0;
@@ -644,7 +660,13 @@ mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s) {
     if (L.n == 8 && noct == 0) lay = 1;                   // pos3 + nrm3 + uv2
     else if (L.n == 7 && noct == 1 && oct0 == 3) lay = 2; // pos3 + oct2 + uv2 (cfg3/cfg4)
     else if (L.n == 3 && noct == 0) lay = 3;              // positions only (cfg2)
-    return dispatch_codec(L.codec, st != nullptr, lay, P, smem, s);
+    bool b16 = true;
+    for (uint32_t c = 0; c < L.n; ++c) b16 = b16 && L.bits[c] == 16;
+    if (lay == 0) {   // generic kernel stages vertex words in smem
+        P.vtx_stage_words = a->d_vertices ? ((L.v_max * L.n_out + 8u + 3u) & ~3u) : 0u;
+        smem += 4u * P.vtx_stage_words;
+    }
+    return dispatch_codec(L.codec, st != nullptr, lay, b16, P, smem, s);
 }
 
 }  // namespace
