@@ -275,7 +275,8 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
             if (lane >= d) { hi1 = max(hi1, o1); hi0 = max(hi0, o0); if (CODEC == MC_CODEC_GTS_REUSE) pc += op; }
         }
         // exclusive: last R / last L strictly before word `lane`, increment flags before it
-        const int prev1 = lane ? __shfl_up_sync(kFull, hi1, 1) : -1;
+        const int prev1_raw = __shfl_up_sync(kFull, hi1, 1);           // every lane shuffles
+        const int prev1 = lane ? prev1_raw : -1;
         const int prev0_raw = __shfl_up_sync(kFull, hi0, 1);
         const int prev0 = lane ? prev0_raw : -1;
         const uint32_t pc_excl_raw = __shfl_up_sync(kFull, pc, 1);
@@ -528,9 +529,11 @@ __global__ void stats_reset_kernel(mc_stats* s) {
 
 // ------------------------------------------------------------------ host launch
 mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t& smem) {
-    if (!a || !a->layout || !a->d_blob || !a->d_indices) return MC_ERR_ARG;
+    if (!a || !a->layout) return MC_ERR_ARG;
     const mc_layout& L = *a->layout;
     if ((uint64_t)a->first + a->count > L.num_meshlets) return MC_ERR_ARG;
+    if (a->count == 0) return MC_OK;                  // nothing to decode (outputs may be empty)
+    if (!a->d_blob || !a->d_indices) return MC_ERR_ARG;
     if (reinterpret_cast<uintptr_t>(a->d_blob) & 15u) return MC_ERR_ARG;
     if ((reinterpret_cast<uintptr_t>(a->d_indices) & 3u) || (reinterpret_cast<uintptr_t>(a->d_vertices) & 15u) ||
         (reinterpret_cast<uintptr_t>(a->d_quantized) & 3u))
