@@ -55,15 +55,15 @@ def log(*a):
 
 # ----------------------------------------------------------------------------- scenes
 
-def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: int):
+def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: int, protos_k=(16, 91)):
     """The rank's shard of the workload as a product-encoded blob (mc_encode path)."""
     w = WORKLOADS[workload]
     if workload == "cfg4_city":
-        scene = synth.city(num_instances=instances * world, num_prototypes=16, k=91, seed=0)
+        scene = synth.city(num_instances=instances * world, num_prototypes=protos_k[0], k=protos_k[1], seed=0)
         protos = [mc.mc_encode(p, w["vmax"], w["tmax"], codec) for p in scene.prototypes]
         blob = mc.mc_blob_instance_range(protos, scene.instance_proto, scene.instance_offset,
                                          rank * instances, instances)
-        meta = {"instances_per_gpu": instances, "prototypes": 16,
+        meta = {"instances_per_gpu": instances, "prototypes": protos_k[0],
                 "restarts_per_meshlet": round(sum(p.encode_stats()["restarts"] for p in protos) /
                                               max(1, sum(p.layout.num_meshlets for p in protos)), 3)}
         return blob, meta
@@ -87,6 +87,15 @@ def record_real_triangles(data: np.ndarray, m0: int, m1: int) -> int:
     tp = data[d + 9].astype(np.int64) + 1
     r = data[d + 12].astype(np.int64) | (data[d + 13].astype(np.int64) << 8)
     return int((tp - 4 * r).sum())
+
+
+def allreduce_u64_sum(values, dist, device):
+    """All-reduce u64 checksums (FORMAT.md §6): int64 sum wraps mod 2^64 exactly like u64."""
+    import torch
+    t = torch.tensor(np.array(values, dtype=np.uint64).view(np.int64), device=device)
+    if dist is not None:
+        dist.all_reduce(t)
+    return [int(x) for x in t.cpu().numpy().view(np.uint64)]
 
 
 # ----------------------------------------------------------------------------- oracle timing (CPU)
@@ -289,13 +298,10 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- verification after timing: checksum all-reduce (the only collective)
     st = db.decode_stats(stream=stream)
-    cs = torch.tensor(np.array([st["checksum_indices"], st["checksum_vertices"]], np.uint64).view(np.int64),
-                      device=dev)
+    checksum = allreduce_u64_sum([st["checksum_indices"], st["checksum_vertices"]], dist, dev)
     errs = torch.tensor([st["error_bits"]], dtype=torch.int64, device=dev)
     if dist:
-        dist.all_reduce(cs)       # int64 sum wraps mod 2^64 == FORMAT.md §6 checksum
         dist.all_reduce(errs)
-    checksum = [int(np.int64(x).view(np.uint64)) for x in cs.cpu().numpy()]
 
     # ---------------- end to end through the C ABI with pinned HOST buffers
     e2e = None

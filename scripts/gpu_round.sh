@@ -1,6 +1,7 @@
 set -x
 mkdir -p gpurun_out
-timeout 300 compute-sanitizer --tool memcheck python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -15
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
-timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench2.json 2> gpurun_out/bench2.err; tail -3 gpurun_out/bench2.err; cat gpurun_out/bench2.json
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:mc_decode_kernel -s 3 -c 1 -o gpurun_out/prof2 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu2.log 2>&1; tail -2 gpurun_out/ncu2.log
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -8
+timeout 900 python bench.py > gpurun_out/bench3.json 2> gpurun_out/bench3.err; tail -3 gpurun_out/bench3.err; cat gpurun_out/bench3.json
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ref3.json 2> gpurun_out/ref3.err; tail -2 gpurun_out/ref3.err; cat gpurun_out/ref3.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches3.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; grep -c mc_decode gpurun_out/launches3.csv
+nproc; lscpu | grep "Model name"

@@ -255,7 +255,7 @@ def test_malformed_streams_flagged(mc, orc):
             assert nb > 0
             b[r["offset"] + r["hdr"] + 8 * W] = 250
         elif what == "size":
-            b[r["offset"] + 9] = (r["Tp"] - 1) + 40 if r["Tp"] + 40 <= 48 else 0
+            b[r["offset"] + 8] = (r["V"] - 1) + 5           # 5 more vertices: +80 B of attributes
         elif what == "object":
             b[r["offset"] + 10] = 7
         err, errs, *_ = orc.decode(b)
