@@ -1,30 +1,33 @@
 // decode.cu — the hot path of libmc: per-meshlet decompression on sm_100a (B200).
 //
-// Paper: arXiv 2404.06359 §4.2–4.4.  One WARP decodes one meshlet record
-// (FORMAT.md) at a time and loops over records with a grid stride:
+// Paper: arXiv 2404.06359 §4.2–4.4.  A GROUP of G lanes decodes one meshlet record
+// (FORMAT.md) at a time and loops over records with a grid stride.  G = 16 by default:
+// each half-warp is an independent group with its own staging buffers, mbarriers and
+// lane mask, so the per-meshlet uniform work (header, validation, flag-word scans,
+// staging) is shared by two meshlets per warp instruction:
 //
 //   a1/a2  the record (header + L/R flags + increment flags + bytes + packed
 //          attributes) is staged HBM -> shared memory with ONE TMA 1-D bulk copy
-//          (cp.async.bulk ... mbarrier::complete_tx), double-buffered per warp so
+//          (cp.async.bulk ... mbarrier::complete_tx), double-buffered per group so
 //          record i+1 is in flight while record i decodes;
 //   a3     index expansion: per-word __popc of the increment flags, an
-//          exclusive warp scan over <= 8 words (__shfl), then
+//          exclusive group scan over <= 8 words (__shfl), then
 //          N[t+2] = i_t ? 2 + c_t : reuse[t - c_t - 1]      ("countbits");
 //   a4     L/R lookback by bit scan: j(t) = max{k<t: f_k != f_t} via
-//          31 - __clz((f_t ? ~w : w) & below(t)) over the current and earlier
-//          words ("firstbithigh", multi-word fallback);
+//          31 - __clz((f_t ? ~w : w) & below(t)) in the current word, earlier words
+//          through per-word last-R / last-L max-scans ("firstbithigh");
 //   a5     triangle assembly with winding-preserving orientation (FORMAT.md §2);
-//   a6     index words staged in smem at the destination's 16-B phase, then
-//          written with coalesced 128-bit stores;
-//   a7/a8  attribute unpack by __funnelshift_r, q = L + code, fp32 via
-//          __fmaf_rn(__uint2float_rn(q), Δ, g), octahedral normals
-//          with IEEE-exact div/sqrt (FORMAT.md §4.3);
+//   a6     index words stored directly (3 x u32 per lane, streaming .cs stores);
+//   a7/a8  attribute unpack (aligned halfwords at b = 16, else a bit reader),
+//          q = L + code, fp32 via __fmaf_rn(__uint2float_rn(q), Δ, g),
+//          octahedral normals with IEEE-exact sqrt/reciprocal (FORMAT.md §4.3);
 //   a9     vertex words stored with 128-bit stores (direct when n_out % 4 == 0,
 //          else through the phase-aligned smem stage);
-//   a10    (stats kernel only) checksums/counters, warp-reduced, one atomic per warp.
+//   a10    (stats kernel only) checksums/counters, group-reduced, one atomic per group.
 //
 // No tensor cores: the path is integer bit manipulation plus one FMA per
 // channel, bound by HBM bandwidth.  No --use_fast_math.
+// Compile-time knobs (MC_*) below exist for A/B experiments (scripts/build_variants.sh).
 #include "../../include/mc.h"
 
 #include <cuda_runtime.h>
@@ -32,6 +35,24 @@
 
 #include <mutex>
 
+#ifndef MC_MIN_BLOCKS
+#define MC_MIN_BLOCKS 1
+#endif
+#ifndef MC_ST_CS
+#define MC_ST_CS 1
+#endif
+#ifndef MC_GROUP16_TMAX
+#define MC_GROUP16_TMAX 256
+#endif
+#ifndef MC_GROUP8
+#define MC_GROUP8 0
+#endif
+#ifndef MC_CONTIG
+#define MC_CONTIG 0
+#endif
+#ifndef MC_MAX_CTAS_PER_SM
+#define MC_MAX_CTAS_PER_SM 64
+#endif
 namespace {
 
 constexpr int kWarpsPerCta = 8;
@@ -104,9 +125,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+#if MC_ST_CS
+#define MC_ST "st.global.cs"
+#else
+#define MC_ST "st.global"
+#endif
 __device__ __forceinline__ void st_v4(uint32_t* p, uint4 v) {
-    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+    asm volatile(MC_ST ".v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
+}
+__device__ __forceinline__ void st_u32(uint32_t* p, uint32_t v) {
+    asm volatile(MC_ST ".u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -118,17 +147,18 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return z;
 }
 
-// Warp-cooperative store of `nwords` u32 from smem to global.  `src` was written at
-// the destination's 16-B phase: src[k] holds dst[k] and (src + head) is 16-B aligned.
-__device__ __forceinline__ void warp_store_words(uint32_t* dst, const uint32_t* src, uint32_t nwords, int lane) {
+// Group-cooperative store of `nwords` u32 from smem to global (G lanes).  `src` was
+// written at the destination's 16-B phase: src[k] holds dst[k] and (src + head) is 16-B aligned.
+template <int G>
+__device__ __forceinline__ void group_store_words(uint32_t* dst, const uint32_t* src, uint32_t nwords, int gl) {
     const uint32_t head = umin((4u - ((uint32_t)(reinterpret_cast<uintptr_t>(dst) >> 2) & 3u)) & 3u, nwords);
-    if ((uint32_t)lane < head) dst[lane] = src[lane];
+    if ((uint32_t)gl < head) st_u32(dst + gl, src[gl]);
     const uint32_t body = (nwords - head) >> 2;
     const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
     uint32_t* d = dst + head;
-    for (uint32_t i = lane; i < body; i += 32) st_v4(d + 4 * i, s4[i]);
+    for (uint32_t i = gl; i < body; i += G) st_v4(d + 4 * i, s4[i]);
     const uint32_t tail = (nwords - head) & 3u;
-    if ((uint32_t)lane < tail) d[4 * body + lane] = src[head + 4 * body + lane];
+    if ((uint32_t)gl < tail) st_u32(d + 4 * body + gl, src[head + 4 * body + gl]);
 }
 
 // FORMAT.md §4.3 octahedral decode, IEEE binary32 RN, no contraction.
@@ -155,44 +185,60 @@ struct WarpStats {
 
 
 // ------------------------------------------------------------------ the kernel
+// G: lanes per meshlet (32 = one warp per meshlet, 16 = two meshlets per warp, each
+// half-warp an independent "group" with its own staging buffers, barriers and lane
+// masks; halves the per-meshlet uniform work (header, scans, staging) per warp).
 // NCH > 0: compile-time channel count (register arrays, static indexing), OCT0 = first
 // channel of the octahedral pair or -1; B16: every channel is 16 bits wide (the paper's
 // b = 16) so codes are read as aligned halfwords.  NCH == 0: generic
 // runtime layout (any n <= 16, widths 1..24, any octahedral placement).
-template <int CODEC, bool STATS, int NCH, int OCT0, bool B16>
-__global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_constant__ Params P) {
+template <int G, int CODEC, bool STATS, int NCH, int OCT0, bool B16>
+__global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(const __grid_constant__ Params P) {
+    static_assert(G == 8 || G == 16 || G == 32, "group size");
+    constexpr int NG = 32 / G;                      // groups (meshlets in flight) per warp
     constexpr int NOUT = NCH > 0 ? NCH + (OCT0 >= 0 ? 1 : 0) : 1;
     const uint32_t n_out = NCH > 0 ? (uint32_t)NOUT : P.n_out;
     extern __shared__ __align__(128) uint8_t smem_raw[];
     const int lane = threadIdx.x & 31;
-    const int wid = threadIdx.x >> 5;
+    const int gl = lane & (G - 1);                  // lane inside the group
+    const int gid = lane / G;
+    const uint32_t gm = G == 32 ? kFull : (((1u << G) - 1u) << (G * gid));   // the group's lane mask
     const uint32_t wpc = blockDim.x >> 5;
-    const uint32_t lt_mask = (1u << lane) - 1u;        // lanes below
-    const uint32_t le_mask = 0xFFFFFFFFu >> (31 - lane);  // lanes at or below
+    const uint32_t gslot = (threadIdx.x >> 5) * NG + gid;             // group slot in the CTA
 
-    // per-warp smem carve-up (all offsets multiples of 16 B)
-    const uint32_t warp_words = 2 * P.buf_words + P.vtx_stage_words + kMiscWords;
-    uint32_t* wbase = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)wid * warp_words;
-    uint32_t* buf0 = wbase;
-    uint32_t* vtx_stage = wbase + 2 * P.buf_words;
+    // per-group smem carve-up (all offsets multiples of 16 B)
+    const uint32_t grp_words = 2 * P.buf_words + P.vtx_stage_words + kMiscWords;
+    uint32_t* gbase = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)gslot * grp_words;
+    uint32_t* buf0 = gbase;
+    uint32_t* vtx_stage = gbase + 2 * P.buf_words;
     uint32_t* misc = vtx_stage + P.vtx_stage_words;
     uint64_t* bars = reinterpret_cast<uint64_t*>(misc);               // 2 mbarriers
     uint32_t* sizes = misc + 4;                                       // staged bytes per buffer
     float* consts = reinterpret_cast<float*>(misc + 8);               // Δ[16], g[16] (generic path)
     uint8_t* Nbuf = reinterpret_cast<uint8_t*>(misc + 40);            // N[0..T'+1], 272 B
 
-    const uint32_t nwarps = gridDim.x * wpc;
-    uint32_t m = P.first + blockIdx.x * wpc + wid;
+    const uint32_t ngroups = gridDim.x * wpc * NG;
+    const uint32_t gg = blockIdx.x * wpc * NG + gslot;
+#if MC_CONTIG
+    // contiguous record range per group
+    const uint32_t per = (P.end - P.first + ngroups - 1) / ngroups;
+    uint32_t m = P.first + min(gg * per, P.end - P.first);
+    const uint32_t mstop = min(P.end, m + per), mstep = 1;
+#else
+    // grid stride: neighbouring groups decode neighbouring records
+    uint32_t m = P.first + gg;
+    const uint32_t mstop = P.end, mstep = ngroups;
+#endif
 
-    if (lane == 0) {
+    if (gl == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         fence_mbar_init();
     }
-    __syncwarp();
+    __syncwarp(gm);
 
-    // a2: lane 0 stages record `mm` with one TMA bulk copy into buffer `b` (or a plain
-    // arrive for a record that cannot be staged: size 0 -> RECORD error)
+    // a2: lane 0 of the group stages record `mm` with one TMA bulk copy into buffer `b`
+    // (or a plain arrive for a record that cannot be staged: size 0 -> RECORD error)
     auto issue = [&](uint32_t d0, uint32_t d1, int b) {
         const uint64_t off = 16ull * d0;
         const uint32_t bytes = (d1 > d0) ? 16u * (d1 - d0) : 0u;
@@ -208,23 +254,23 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
     };
 
     uint32_t nd0 = 0, nd1 = 0;   // directory entries of the record after next (prefetched)
-    if (m < P.end && lane == 0) {
+    if (m < mstop && gl == 0) {
         issue(__ldg(P.dir + m), __ldg(P.dir + m + 1), 0);
-        if (m + nwarps < P.end) { nd0 = __ldg(P.dir + m + nwarps); nd1 = __ldg(P.dir + m + nwarps + 1); }
+        if (m + mstep < mstop) { nd0 = __ldg(P.dir + m + mstep); nd1 = __ldg(P.dir + m + mstep + 1); }
     }
 
     WarpStats ws;
     uint32_t k = 0;
-    for (; m < P.end; m += nwarps, ++k) {
+    for (; m < mstop; m += mstep, ++k) {
         const int b = k & 1;
-        const uint32_t mnext = m + nwarps;
-        if (lane == 0 && mnext < P.end) {
+        const uint32_t mnext = m + mstep;
+        if (gl == 0 && mnext < mstop) {
             issue(nd0, nd1, b ^ 1);
-            const uint32_t m2 = mnext + nwarps;
-            if (m2 < P.end) { nd0 = __ldg(P.dir + m2); nd1 = __ldg(P.dir + m2 + 1); }
+            const uint32_t m2 = mnext + mstep;
+            if (m2 < mstop) { nd0 = __ldg(P.dir + m2); nd1 = __ldg(P.dir + m2 + 1); }
         }
         mbar_wait(&bars[b], (k >> 1) & 1);
-        __syncwarp();
+        __syncwarp(gm);
         const uint32_t* R = buf0 + (size_t)b * P.buf_words;
         const uint32_t staged = sizes[b];
 
@@ -250,59 +296,62 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
         const uint8_t* BY = reinterpret_cast<const uint8_t*>(R + by_w);
         const uint32_t* AT = R + at_w;
 
-        // ---------------- per-word prefix state, lanes 0..W-1 hold word `lane` (W <= 8)
-        // valid bits of word `lane`: triangles t < T', bit 0 (t = 0) excluded
+        // ---------------- per-word prefix state, group lanes 0..W-1 hold word `gl` (W <= 8)
+        // valid bits of word `gl`: triangles t < T', bit 0 (t = 0) excluded
         uint32_t vm = 0;
-        if ((uint32_t)lane < W) {
-            const uint32_t rem = Tp - 32u * lane;
+        if ((uint32_t)gl < W) {
+            const uint32_t rem = Tp - 32u * gl;
             vm = rem >= 32u ? 0xFFFFFFFFu : ((1u << rem) - 1u);
         }
-        if (lane == 0) vm &= ~1u;
-        const uint32_t lrw = ((uint32_t)lane < W && !err) ? (R[lr_w + lane] & vm) : 0u;      // f_0 := L
+        if (gl == 0) vm &= ~1u;
+        const uint32_t lrw = ((uint32_t)gl < W && !err) ? (R[lr_w + gl] & vm) : 0u;      // f_0 := L
         // highest R (1) and highest L (0) flag position in this word (bit 0 of word 0 is L)
-        const uint32_t ones = lrw, zeros = (~lrw & vm) | (lane == 0 ? 1u : 0u);
-        int hi1 = ones ? 32 * lane + 31 - __clz(ones) : -1;
-        int hi0 = ((uint32_t)lane < W && zeros) ? 32 * lane + 31 - __clz(zeros) : -1;
+        const uint32_t ones = lrw, zeros = (~lrw & vm) | (gl == 0 ? 1u : 0u);
+        int hi1 = ones ? 32 * gl + 31 - __clz(ones) : -1;
+        int hi0 = ((uint32_t)gl < W && zeros) ? 32 * gl + 31 - __clz(zeros) : -1;
         uint32_t incw = 0, pc = 0;
         if (CODEC == MC_CODEC_GTS_REUSE) {
-            incw = ((uint32_t)lane < W && !err) ? (R[inc_w + lane] & vm) : 0u;
+            incw = ((uint32_t)gl < W && !err) ? (R[inc_w + gl] & vm) : 0u;
             pc = __popc(incw);
         }
 #pragma unroll
         for (int d = 1; d < 8; d <<= 1) {           // inclusive max / add scans over <= 8 words
-            const int o1 = __shfl_up_sync(kFull, hi1, d), o0 = __shfl_up_sync(kFull, hi0, d);
-            const uint32_t op = __shfl_up_sync(kFull, pc, d);
-            if (lane >= d) { hi1 = max(hi1, o1); hi0 = max(hi0, o0); if (CODEC == MC_CODEC_GTS_REUSE) pc += op; }
+            const int o1 = __shfl_up_sync(gm, hi1, d, G), o0 = __shfl_up_sync(gm, hi0, d, G);
+            const uint32_t op = __shfl_up_sync(gm, pc, d, G);
+            if (gl >= d) { hi1 = max(hi1, o1); hi0 = max(hi0, o0); if (CODEC == MC_CODEC_GTS_REUSE) pc += op; }
         }
-        // exclusive: last R / last L strictly before word `lane`, increment flags before it
-        const int prev1_raw = __shfl_up_sync(kFull, hi1, 1);           // every lane shuffles
-        const int prev1 = lane ? prev1_raw : -1;
-        const int prev0_raw = __shfl_up_sync(kFull, hi0, 1);
-        const int prev0 = lane ? prev0_raw : -1;
-        const uint32_t pc_excl_raw = __shfl_up_sync(kFull, pc, 1);
-        const uint32_t pc_excl = lane ? pc_excl_raw : 0u;
+        // exclusive: last R / last L strictly before word `gl`, increment flags before it
+        const int prev1_raw = __shfl_up_sync(gm, hi1, 1, G);          // every lane shuffles
+        const int prev1 = gl ? prev1_raw : -1;
+        const int prev0_raw = __shfl_up_sync(gm, hi0, 1, G);
+        const int prev0 = gl ? prev0_raw : -1;
+        const uint32_t pc_excl_raw = __shfl_up_sync(gm, pc, 1, G);
+        const uint32_t pc_excl = gl ? pc_excl_raw : 0u;
         if (CODEC == MC_CODEC_GTS_REUSE) {
-            const uint32_t total = __shfl_sync(kFull, pc, 7);
+            const uint32_t total = __shfl_sync(gm, pc, 7, G);
             if (!err && total != V - 3u) err |= MC_DERR_COUNTS;
         }
         if (err) {
-            if (STATS && lane == 0) {
+            if (STATS && gl == 0) {
                 atomicOr(&P.stats->error_bits, err);
                 atomicMin(&P.stats->first_bad_meshlet, m);
                 atomicAdd(&P.stats->num_bad, 1u);
             }
-            __syncwarp();
+            __syncwarp(gm);
             continue;
         }
 
-        // ---------------- a3/a4/a5/a6: topology, one triangle per lane per word
-        if (lane < 2) Nbuf[lane] = (uint8_t)lane;                            // N[0], N[1]
+        // ---------------- a3/a4/a5/a6: topology, one triangle per lane, G per step
+        if (gl < 2) Nbuf[gl] = (uint8_t)gl;                                  // N[0], N[1]
         const uint32_t vout = vtx_base - P.index_sub;
         uint32_t* idst = P.idx + 3ull * (tri_base - P.base_tri);
-        uint32_t carry = 2u;                                                 // N[t+1] for lane 0
+        uint32_t carry = 2u;                                                 // N[t+1] for group lane 0
         uint32_t e2 = 0;
-        for (uint32_t j = 0; j < W; ++j) {
-            const uint32_t t = 32u * j + lane;
+        const uint32_t nsteps = (Tp + G - 1) / G;
+        for (uint32_t j = 0; j < nsteps; ++j) {
+            const uint32_t t = G * j + gl;
+            const uint32_t wj = (G * j) >> 5;                                // flag word of this step
+            const uint32_t bit = t & 31u;
             const bool active = t < Tp;
             // a3: new-vertex index N[t+2] (w_0 := N[2] = 2)
             uint32_t w = 2u;
@@ -310,9 +359,9 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
                 if (active && t >= 1u) w = BY[t - 1u];
                 if (STATS && active && w >= V) e2 |= MC_DERR_INDEX;
             } else {
-                const uint32_t iw = __shfl_sync(kFull, incw, j);
-                const uint32_t c = __shfl_sync(kFull, pc_excl, j) + __popc(iw & le_mask);   // inclusive scan c_t
-                if ((iw >> lane) & 1u) w = 2u + c;
+                const uint32_t iw = __shfl_sync(gm, incw, wj, G);
+                const uint32_t c = __shfl_sync(gm, pc_excl, wj, G) + __popc(iw & (0xFFFFFFFFu >> (31u - bit)));   // inclusive c_t
+                if ((iw >> bit) & 1u) w = 2u + c;
                 else if (active && t >= 1u) {
                     w = BY[t - c - 1u];                                      // location t+1-s, s = 2+c
                     if (STATS && w >= V) e2 |= MC_DERR_REUSE;
@@ -321,36 +370,36 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
             if (active) Nbuf[t + 2u] = (uint8_t)w;
             // a4: j(t) = max{k < t : f_k != f_t} by bit scan; earlier words
             // through the per-word last-R / last-L scans instead of a loop
-            const uint32_t lw = __shfl_sync(kFull, lrw, j);
-            const int p1 = __shfl_sync(kFull, prev1, j), p0 = __shfl_sync(kFull, prev0, j);
-            const uint32_t nprev_up = __shfl_up_sync(kFull, w, 1);
-            const uint32_t nprev = lane ? nprev_up : carry;                  // N[t+1]
-            carry = __shfl_sync(kFull, w, 31);
-            __syncwarp();
+            const uint32_t lw = __shfl_sync(gm, lrw, wj, G);
+            const int p1 = __shfl_sync(gm, prev1, wj, G), p0 = __shfl_sync(gm, prev0, wj, G);
+            const uint32_t nprev_up = __shfl_up_sync(gm, w, 1, G);
+            const uint32_t nprev = gl ? nprev_up : carry;                    // N[t+1]
+            carry = __shfl_sync(gm, w, G - 1, G);
+            __syncwarp(gm);
             if (active) {
-                const uint32_t f = (lw >> lane) & 1u;
-                const uint32_t x = (f ? ~lw : lw) & lt_mask;
-                const int jj = x ? (int)(32u * j) + 31 - __clz(x) : (f ? p0 : p1);
+                const uint32_t f = (lw >> bit) & 1u;
+                const uint32_t x = (f ? ~lw : lw) & ((1u << bit) - 1u);
+                const int jj = x ? (int)(32u * wj) + 31 - __clz(x) : (f ? p0 : p1);
                 const uint32_t npiv = Nbuf[jj + 1];                          // N[j+1], N[0] if none
                 uint32_t a0 = f ? nprev : npiv, a1 = f ? npiv : nprev;       // a5 (FORMAT.md §2)
                 if (t == 0) { a0 = 0u; a1 = 1u; }
                 const uint32_t o0 = vout + a0, o1 = vout + a1, o2 = vout + w;
                 uint32_t* d = idst + 3u * t;                                 // a6
-                d[0] = o0;
-                d[1] = o1;
-                d[2] = o2;
+                st_u32(d, o0);
+                st_u32(d + 1, o1);
+                st_u32(d + 2, o2);
                 if (STATS) {
                     const uint64_t kk = 3ull * ((uint64_t)tri_base + t);
                     ws.cs_idx += mix64((kk << 32) | o0) + mix64(((kk + 1) << 32) | o1) + mix64(((kk + 2) << 32) | o2);
                     ws.degen += (a0 == a1 || a1 == w || a0 == w) ? 1u : 0u;
                     if (t > 0) ws.max_lb = max(ws.max_lb, (uint32_t)((int)t - jj));
-                    if (t > 0 && !x && j > 0) ws.multi++;
+                    if (t > 0 && !x && wj > 0) ws.multi++;
                 }
             }
         }
         if (STATS) {
-            e2 = __reduce_or_sync(kFull, e2);
-            if (lane == 0) {
+            e2 = __reduce_or_sync(gm, e2);
+            if (gl == 0) {
                 ws.tris += Tp;
                 ws.verts += V;
                 if (e2) {
@@ -368,16 +417,26 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
             float* fdst = want_f ? P.fout + (size_t)n_out * vpos : nullptr;
             if constexpr (NCH > 0) {
                 // per-meshlet grid constants in registers: Δ_c, g_c, L_c
-                const float cv = (uint32_t)lane < 2u * NCH ? __ldg(P.objtab + (size_t)object * 2u * NCH + lane) : 0.0f;
                 float dl[NCH], og[NCH];
                 uint32_t Lc[NCH];
+                const float* ot = P.objtab + (size_t)object * 2u * NCH;
+                if constexpr (2 * NCH <= G) {   // one constant per group lane, then broadcast
+                    const float cv = (uint32_t)gl < 2u * NCH ? __ldg(ot + gl) : 0.0f;
 #pragma unroll
-                for (int c = 0; c < NCH; ++c) {
-                    dl[c] = __shfl_sync(kFull, cv, c);
-                    og[c] = __shfl_sync(kFull, cv, NCH + c);
-                    Lc[c] = R[4 + c];
+                    for (int c = 0; c < NCH; ++c) {
+                        dl[c] = __shfl_sync(gm, cv, c, G);
+                        og[c] = __shfl_sync(gm, cv, NCH + c, G);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) {
+                        dl[c] = __ldg(ot + c);
+                        og[c] = __ldg(ot + NCH + c);
+                    }
                 }
-                for (uint32_t v = lane; v < V; v += 32) {
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) Lc[c] = R[4 + c];
+                for (uint32_t v = gl; v < V; v += G) {
                     uint32_t qv[NCH];
                     if constexpr (B16) {
                         const uint16_t* H = reinterpret_cast<const uint16_t*>(AT) + (size_t)v * NCH;
@@ -403,7 +462,7 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
                         uint32_t* qd = P.qout + (size_t)NCH * (vpos + v);
 #pragma unroll
                         for (int c = 0; c < NCH; ++c) {
-                            qd[c] = qv[c];
+                            st_u32(qd + c, qv[c]);
                             if (STATS) ws.cs_q += mix64((((uint64_t)NCH * (vtx_base + v) + c) << 32) | qv[c]);
                         }
                     }
@@ -434,17 +493,17 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
                                                          __float_as_uint(outv[k2 + 2]), __float_as_uint(outv[k2 + 3])));
                         } else {
 #pragma unroll
-                            for (int k2 = 0; k2 < NOUT; ++k2) d[k2] = __float_as_uint(outv[k2]);
+                            for (int k2 = 0; k2 < NOUT; ++k2) st_u32(d + k2, __float_as_uint(outv[k2]));
                         }
                     }
                 }
             } else {
                 // generic layout: runtime channel loop, outputs through the smem stage
-                if ((uint32_t)lane < 2u * P.n) consts[lane] = __ldg(P.objtab + (size_t)object * 2u * P.n + lane);
-                __syncwarp();
+                for (uint32_t i = gl; i < 2u * P.n; i += G) consts[i] = __ldg(P.objtab + (size_t)object * 2u * P.n + i);
+                __syncwarp(gm);
                 const uint32_t fphase = want_f ? ((uint32_t)(reinterpret_cast<uintptr_t>(fdst) >> 2) & 3u) : 0u;
                 uint32_t* vst = vtx_stage + fphase;
-                for (uint32_t v = lane; v < V; v += 32) {
+                for (uint32_t v = gl; v < V; v += G) {
                     const uint32_t bit0 = v * P.S;
                     const uint32_t* wp = AT + (bit0 >> 5);
                     uint64_t acc = (uint64_t)(wp[0] >> (bit0 & 31u));
@@ -459,7 +518,7 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
                         acc >>= bb;
                         avail -= bb;
                         if (want_q) {
-                            qd[c] = q;
+                            st_u32(qd + c, q);
                             if (STATS) ws.cs_q += mix64((((uint64_t)P.n * (vtx_base + v) + c) << 32) | q);
                         }
                         if (!want_f) continue;
@@ -485,25 +544,25 @@ __global__ void __launch_bounds__(kThreads) mc_decode_kernel(const __grid_consta
                     }
                 }
                 if (want_f) {
-                    __syncwarp();
-                    warp_store_words(reinterpret_cast<uint32_t*>(fdst), vst, n_out * V, lane);
+                    __syncwarp(gm);
+                    group_store_words<G>(reinterpret_cast<uint32_t*>(fdst), vst, n_out * V, gl);
                 }
             }
         }
-        __syncwarp();
+        __syncwarp(gm);
     }
 
     if (STATS) {
-        // a10: warp reduction, one atomic per counter per warp
-        for (int d = 16; d > 0; d >>= 1) {
-            ws.cs_idx += __shfl_down_sync(kFull, ws.cs_idx, d);
-            ws.cs_f += __shfl_down_sync(kFull, ws.cs_f, d);
-            ws.cs_q += __shfl_down_sync(kFull, ws.cs_q, d);
-            ws.degen += __shfl_down_sync(kFull, ws.degen, d);
-            ws.multi += __shfl_down_sync(kFull, ws.multi, d);
-            ws.max_lb = max(ws.max_lb, __shfl_down_sync(kFull, ws.max_lb, d));
+        // a10: group reduction, one atomic per counter per group
+        for (int d = G / 2; d > 0; d >>= 1) {
+            ws.cs_idx += __shfl_down_sync(gm, ws.cs_idx, d, G);
+            ws.cs_f += __shfl_down_sync(gm, ws.cs_f, d, G);
+            ws.cs_q += __shfl_down_sync(gm, ws.cs_q, d, G);
+            ws.degen += __shfl_down_sync(gm, ws.degen, d, G);
+            ws.multi += __shfl_down_sync(gm, ws.multi, d, G);
+            ws.max_lb = max(ws.max_lb, __shfl_down_sync(gm, ws.max_lb, d, G));
         }
-        if (lane == 0) {
+        if (gl == 0) {
             atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->checksum_indices), ws.cs_idx);
             atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->checksum_vertices), ws.cs_f);
             atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->checksum_quantized), ws.cs_q);
@@ -585,13 +644,15 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
         }
     }
     const uint32_t warp_words = 2 * P.buf_words + P.vtx_stage_words + kMiscWords;
-    smem = (size_t)warp_words * 4u;   // per warp; the launch multiplies by warps per CTA
+    smem = (size_t)warp_words * 4u;   // per group; the launch multiplies by groups per CTA
     return MC_OK;
 }
 
-template <int CODEC, bool STATS, int NCH, int OCT0, bool B16>
-mc_status launch_t(const Params& P, size_t warp_smem, cudaStream_t s) {
-    auto kern = mc_decode_kernel<CODEC, STATS, NCH, OCT0, B16>;
+template <int G, int CODEC, bool STATS, int NCH, int OCT0, bool B16>
+mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
+    auto kern = mc_decode_kernel<G, CODEC, STATS, NCH, OCT0, B16>;
+    constexpr uint32_t NG = 32 / G;
+    const size_t warp_smem = NG * grp_smem;
     // warps per CTA: 8, fewer when a warp's staging buffers are large (Ṽ=T̃=256, 24-bit)
     const size_t budget = 200u * 1024u;
     uint32_t wpc = (uint32_t)std::min<size_t>(kWarpsPerCta, std::max<size_t>(1, budget / warp_smem));
@@ -622,11 +683,22 @@ mc_status launch_t(const Params& P, size_t warp_smem, cudaStream_t s) {
         bps_cache[wpc][bucket] = bps;
     }
     const uint32_t count = P.end - P.first;
-    const uint64_t want = (count + wpc - 1) / wpc;
-    const uint64_t cap = (uint64_t)sms * bps;
+    const uint64_t want = (count + wpc * NG - 1) / (wpc * NG);
+    const uint64_t cap = (uint64_t)sms * std::min(bps, MC_MAX_CTAS_PER_SM);
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
     kern<<<grid, 32 * wpc, smem, s>>>(P);
     return cudaGetLastError() == cudaSuccess ? MC_OK : MC_ERR_CUDA;
+}
+
+// group size: two meshlets per warp (G = 16) when a meshlet has at most
+// MC_GROUP16_TMAX decoded triangles, else one meshlet per warp (G = 32)
+template <int CODEC, bool STATS, int NCH, int OCT0, bool B16>
+mc_status launch_t(const Params& P, size_t grp_smem, cudaStream_t s) {
+#if MC_GROUP8
+    if (P.tmax <= MC_GROUP16_TMAX) return launch_g<8, CODEC, STATS, NCH, OCT0, B16>(P, grp_smem, s);
+#endif
+    if (P.tmax <= MC_GROUP16_TMAX) return launch_g<16, CODEC, STATS, NCH, OCT0, B16>(P, grp_smem, s);
+    return launch_g<32, CODEC, STATS, NCH, OCT0, B16>(P, grp_smem, s);
 }
 
 template <int CODEC, bool STATS>
