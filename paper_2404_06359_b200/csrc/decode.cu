@@ -47,6 +47,9 @@
 #ifndef MC_GROUP8
 #define MC_GROUP8 0
 #endif
+#ifndef MC_BANK_PAD
+#define MC_BANK_PAD 1
+#endif
 #ifndef MC_CONTIG
 #define MC_CONTIG 0
 #endif
@@ -72,6 +75,7 @@ struct Params {
     uint32_t hdr_words;        // record header words (16 + 4n rounded to 16) / 4
     uint32_t buf_words;        // per-buffer words (max_rec/4 + 4)
     uint32_t vtx_stage_words;  // vmax*n_out + 8 for the generic layout, else 0
+    uint32_t grp_words;        // smem words per group: 2 buffers + vertex stage + misc, padded
     uint32_t* idx;
     float* fout;
     uint32_t* qout;
@@ -207,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
     const uint32_t gslot = (threadIdx.x >> 5) * NG + gid;             // group slot in the CTA
 
     // per-group smem carve-up (all offsets multiples of 16 B)
-    const uint32_t grp_words = 2 * P.buf_words + P.vtx_stage_words + kMiscWords;
+    const uint32_t grp_words = P.grp_words;
     uint32_t* gbase = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)gslot * grp_words;
     uint32_t* buf0 = gbase;
     uint32_t* vtx_stage = gbase + 2 * P.buf_words;
@@ -643,8 +647,7 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
             col += 1;
         }
     }
-    const uint32_t warp_words = 2 * P.buf_words + P.vtx_stage_words + kMiscWords;
-    smem = (size_t)warp_words * 4u;   // per group; the launch multiplies by groups per CTA
+    smem = 0;   // per group, set by launch() once the vertex stage is known
     return MC_OK;
 }
 
@@ -737,10 +740,13 @@ mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s) {
     else if (L.n == 3 && noct == 0) lay = 3;              // positions only (cfg2)
     bool b16 = true;
     for (uint32_t c = 0; c < L.n; ++c) b16 = b16 && L.bits[c] == 16;
-    if (lay == 0) {   // generic kernel stages vertex words in smem
+    if (lay == 0)   // generic kernel stages vertex words in smem
         P.vtx_stage_words = a->d_vertices ? ((L.v_max * L.n_out + 8u + 3u) & ~3u) : 0u;
-        smem += 4u * P.vtx_stage_words;
-    }
+    // group stride = 16 (mod 32) words: the two groups of a warp reading the same
+    // record offset hit different banks
+    P.grp_words = 2 * P.buf_words + P.vtx_stage_words + kMiscWords;
+    if (MC_BANK_PAD) P.grp_words += (48u - (P.grp_words & 31u)) & 31u;
+    smem = 4u * (size_t)P.grp_words;
     return dispatch_codec(L.codec, st != nullptr, lay, b16, P, smem, s);
 }
 
