@@ -108,8 +108,10 @@ def host_cores() -> int:
 
 
 def oracle_time(data: np.ndarray, seconds: float, cores: int):
-    """Time the oracle decoder (as it stands) on `cores` host threads over the first S
-    records, S calibrated so the run takes about `seconds`.  Returns (tri/s, S, T, wall)."""
+    """Time the oracle decoder (as it stands) on `cores` host threads: passes over the
+    first S records (S calibrated so one pass takes about `seconds`, capped at the whole
+    workload), repeated until at least `seconds` of wall time have elapsed.
+    Returns (tri/s, S, T, wall, passes) with T the real triangles decoded over all passes."""
     import oracle
     info = oracle.blob_info(data)
     M = info.M
@@ -130,13 +132,19 @@ def oracle_time(data: np.ndarray, seconds: float, cores: int):
     idx = np.zeros(min(tot_tp, 3 * info.total_tp), np.uint32)
     f = np.zeros(info.n_out * min(tot_v, info.total_v), np.float32)
     bounds = np.linspace(0, S, cores * 4 + 1).astype(np.int64)
+    T1 = record_real_triangles(data, 0, S)
+    passes = 0
     t0 = time.perf_counter()
     with ThreadPoolExecutor(cores) as ex:
-        list(ex.map(lambda i: oracle.decode_range_raw(data, int(bounds[i]), int(bounds[i + 1]), idx, None, f),
-                    range(len(bounds) - 1)))
+        while True:
+            list(ex.map(lambda i: oracle.decode_range_raw(data, int(bounds[i]), int(bounds[i + 1]), idx, None, f),
+                        range(len(bounds) - 1)))
+            passes += 1
+            if time.perf_counter() - t0 >= seconds or passes >= 10000:
+                break
     wall = time.perf_counter() - t0
-    T = record_real_triangles(data, 0, S)
-    return T / wall, S, T, wall
+    T = T1 * passes
+    return T / wall, S, T, wall, passes
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -226,10 +234,10 @@ def run_reference(args, rank, world):
     cores = host_cores()
     per_step = max(0.5, min(3.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        oracle_time(data, per_step, cores)
+        oracle_time(data, min(per_step, 1.0), cores)
     rates, walls, tris, recs = [], [], 0, 0
     for _ in range(args.steps):
-        r, S, T, wall = oracle_time(data, per_step, cores)
+        r, S, T, wall, passes = oracle_time(data, per_step, cores)
         rates.append(r)
         walls.append(wall)
         tris += T
@@ -240,7 +248,8 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/fp32",
             "data": "synthetic", "config": {"workload": args.workload, **WORKLOADS[args.workload], **meta},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"first {recs} records of the workload per step (~{per_step:.1f}s of CPU work)"},
+                             "sample": f"per step: {passes} pass(es) over the first {recs} records of the workload "
+                                       f"(>= {per_step:.1f}s of CPU work)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -340,9 +349,10 @@ def run_ours(args, rank, world, local_rank):
         import oracle
         oracle.build()
         cores = host_cores()
-        rate, S, T, wall = oracle_time(np.array(blob.bytes), args.cpu_seconds, cores)
+        rate, S, T, wall, passes = oracle_time(np.array(blob.bytes), args.cpu_seconds, cores)
         cpu = {"value": rate / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"first {S} of {L.num_meshlets} records ({T} tris), {wall:.1f}s wall on {cores} threads"}
+               "sample": f"{passes} pass(es) over the first {S} of {L.num_meshlets} records "
+                         f"({T} tris decoded in total), {wall:.1f}s wall on {cores} threads"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,

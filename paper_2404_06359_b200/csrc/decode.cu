@@ -42,7 +42,7 @@
 #define MC_ST_CS 1
 #endif
 #ifndef MC_GROUP16_TMAX
-#define MC_GROUP16_TMAX 256
+#define MC_GROUP16_TMAX 128
 #endif
 #ifndef MC_GROUP8
 #define MC_GROUP8 0
