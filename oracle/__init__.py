@@ -22,7 +22,7 @@ _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 DERR_RECORD, DERR_COUNTS, DERR_INDEX, DERR_REUSE, DERR_OBJECT = 1, 2, 4, 8, 16
-CODEC_GTS, CODEC_REUSE = 1, 2
+CODEC_GTS, CODEC_REUSE, CODEC_BASIC = 1, 2, 3
 
 
 def build(force: bool = False) -> str:
@@ -49,6 +49,8 @@ def lib():
         L.or_decode_meshlet.restype = u32
         L.or_decode_range.argtypes = [P, sz, u32, u32, P, P, P, P]
         L.or_decode_range.restype = u32
+        L.or_decode_range_u8x4.argtypes = [P, sz, u32, u32, P]
+        L.or_decode_range_u8x4.restype = u32
         L.or_checksum.argtypes = [P, u64, u64]
         L.or_checksum.restype = u64
         L.or_oct_decode.argtypes = [ctypes.c_float, ctypes.c_float, P]
@@ -140,6 +142,15 @@ def decode(blob: np.ndarray, want_q=True, want_f=True, m0=0, m1=None):
     err = np.zeros(max(m1 - m0, 1), np.uint32)
     allerr = lib().or_decode_range(_p(blob), blob.nbytes, m0, m1, _p(idx), _p(q), _p(f), _p(err))
     return int(allerr), err[:m1 - m0], idx, q, f
+
+
+def decode_u8x4(blob: np.ndarray, m0=0, m1=None):
+    """Local u8x4 index words (FORMAT.md §2) of the sequential decode: (err, words[total_tp])."""
+    info = blob_info(blob)
+    m1 = info.M if m1 is None else m1
+    words = np.zeros(max(info.total_tp, 1), np.uint32)
+    err = lib().or_decode_range_u8x4(_p(blob), blob.nbytes, m0, m1, _p(words))
+    return int(err), words[:info.total_tp]
 
 
 def decode_range_raw(blob, m0, m1, idx, q, f):

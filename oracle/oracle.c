@@ -16,6 +16,8 @@
  *     splitting when T' = T + 4R exceeds T~, the ascending vertex
  *     reorder, GTS / GTS-Reuse stream emission (P:420-426,
  *     P:459-467) and the crack-free global-grid quantiser.
+ *   - Basic (codec 3): the paper's uncompressed mesh-shading control — three
+ *     local u8 indices per triangle (Table 2).
  *   - or_pack: serialises caller-given raw streams WITHOUT validation so tests
  *     can build exhaustive and malformed inputs.
  * Floating point: compiled with -ffp-contract=off; every fused multiply-add is an
@@ -48,6 +50,7 @@
 
 #define CODEC_GTS 1u
 #define CODEC_REUSE 2u
+#define CODEC_BASIC 3u   /* three local u8 indices per triangle: the paper's "Basic" */
 #define SEM_OCT 4u
 
 /* ------------------------------------------------------------------ byte access */
@@ -105,7 +108,7 @@ static int parse_header(const uint8_t *b, size_t nbytes, or_hdr *h) {
     h->total_bytes = rd64(b + 88);
     memcpy(h->bits, b + 96, 16);
     memcpy(h->sem, b + 112, 16);
-    if (h->codec != CODEC_GTS && h->codec != CODEC_REUSE) return OR_ERR_FORMAT;
+    if (h->codec != CODEC_GTS && h->codec != CODEC_REUSE && h->codec != CODEC_BASIC) return OR_ERR_FORMAT;
     if (h->n < 1 || h->n > 16 || h->O < 1) return OR_ERR_FORMAT;
     if (h->total_bytes != nbytes) return OR_ERR_FORMAT;
     if (h->off_dir + 4ull * (h->M + 1ull) > nbytes || h->off_obj + 8ull * h->n * h->O > nbytes ||
@@ -183,10 +186,12 @@ uint32_t or_decode_meshlet(const uint8_t *blob, size_t nbytes, uint32_t m, uint3
         meta_out[3] = Tp; meta_out[4] = object; meta_out[5] = R;
     }
     uint32_t n = h.n;
-    uint32_t W = (Tp + 31u) / 32u;
+    /* Basic records have no flag words (FORMAT.md §1.4) */
+    uint32_t W = h.codec == CODEC_BASIC ? 0u : (Tp + 31u) / 32u;
     uint64_t hdr_bytes = up16(16u + 4ull * n);
     uint32_t nb;
     if (h.codec == CODEC_GTS) nb = Tp - 1u;
+    else if (h.codec == CODEC_BASIC) nb = 3u * Tp;
     else nb = (V >= 3u && V - 3u <= Tp - 1u) ? (Tp - 1u) - (V - 3u) : 0u;
     uint64_t off_lr = hdr_bytes;
     uint64_t off_inc = off_lr + 4ull * W;
@@ -198,6 +203,7 @@ uint32_t or_decode_meshlet(const uint8_t *blob, size_t nbytes, uint32_t m, uint3
     if (size != r1 - r0 || size > h.max_record_bytes) return DERR_RECORD;
     if (V < 3u || V > h.vmax || Tp > h.tmax) err |= DERR_COUNTS;
     if (object >= h.O) err |= DERR_OBJECT;
+    if (h.codec == CODEC_BASIC && R != 0u) err |= DERR_COUNTS;   /* Basic has no restarts */
 
     const uint8_t *LR = rec + off_lr, *INC = rec + off_inc, *BY = rec + off_bytes, *AT = rec + off_attr;
 
@@ -212,6 +218,16 @@ uint32_t or_decode_meshlet(const uint8_t *blob, size_t nbytes, uint32_t m, uint3
     /* structural errors (RECORD/COUNTS/OBJECT) end the record: FORMAT.md §5 evaluates
      * INDEX/REUSE only for structurally valid records */
     if (err) return err;
+    if (h.codec == CODEC_BASIC) {
+        /* Basic: the triangle list itself, three local indices per triangle */
+        for (uint32_t t = 0; t < Tp; ++t)
+            for (uint32_t k = 0; k < 3u; ++k) {
+                uint32_t w = BY[3u * t + k];
+                if (w >= V) err |= DERR_INDEX;
+                if (tri_out) tri_out[3u * t + k] = w;
+            }
+        goto attributes;
+    }
     uint32_t c = 0; /* inclusive add-scan of increment flags over triangles 1..t */
     for (uint32_t t = 1; t < Tp; ++t) {
         uint32_t w;
@@ -244,6 +260,7 @@ uint32_t or_decode_meshlet(const uint8_t *blob, size_t nbytes, uint32_t m, uint3
         if (tri_out) { tri_out[3 * t] = a; tri_out[3 * t + 1] = b; tri_out[3 * t + 2] = cc; }
     }
 
+attributes:
     /* Attributes: q = L_i + code on the global grid; x = fmaf((float)q, Δ, g). */
     if ((q_out || f_out) && !(err & (DERR_OBJECT | DERR_COUNTS))) {
         const uint8_t *obj = blob + h.off_obj + 8ull * n * object;
@@ -306,6 +323,29 @@ uint32_t or_decode_range(const uint8_t *blob, size_t nbytes, uint32_t m0, uint32
     return all;
 }
 
+/* Local u8x4 index output (FORMAT.md §2, decode flag MC_DECODE_INDEX_LOCAL_U8X4):
+ * triangle t of record m -> word (tri_base - base_tri + t) = a | b<<8 | c<<16 with the
+ * meshlet-local indices of the sequential decode (the paper's 8-bit meshlet indices).
+ * words: total_tp u32.  Returns the OR of all error bits. */
+uint32_t or_decode_range_u8x4(const uint8_t *blob, size_t nbytes, uint32_t m0, uint32_t m1, uint32_t *words) {
+    or_hdr h;
+    if (parse_header(blob, nbytes, &h) != OR_OK) return DERR_RECORD;
+    uint32_t all = 0;
+    uint32_t tri[3 * 256];
+    for (uint32_t m = m0; m < m1 && m < h.M; ++m) {
+        uint32_t meta[6] = {0};
+        uint32_t e = or_decode_meshlet(blob, nbytes, m, tri, NULL, NULL, meta);
+        all |= e;
+        if (e & (DERR_RECORD | DERR_COUNTS | DERR_OBJECT)) continue;
+        uint64_t tb = (uint64_t)meta[1] - h.base_tri;
+        uint32_t Tp = meta[3];
+        if (tb + Tp > h.total_tp) { all |= DERR_RECORD; continue; }
+        for (uint32_t t = 0; t < Tp; ++t)
+            words[tb + t] = (tri[3 * t] & 0xFFu) | ((tri[3 * t + 1] & 0xFFu) << 8) | ((tri[3 * t + 2] & 0xFFu) << 16);
+    }
+    return all;
+}
+
 /* ------------------------------------------------------------------ checksum (FORMAT.md §6) */
 static uint64_t mix64(uint64_t z) {
     z ^= z >> 30; z *= 0xbf58476d1ce4e5b9ull;
@@ -361,7 +401,28 @@ typedef struct {
     uint8_t f[256];
     uint32_t src_tri[256];
     uint32_t vlist[256];   /* local -> source vertex */
+    uint8_t idx3[768];     /* Basic: local triangle list */
 } emitted;
+
+/* Basic (codec 3): the meshlet's triangles in growth order, local vertices numbered by
+ * first appearance (FORMAT.md §1.4), no strips, no restarts. */
+static int emit_basic(const uint32_t *I, const uint32_t *tris, uint32_t nt, emitted *em, int32_t *vlocal) {
+    uint32_t V = 0;
+    for (uint32_t t = 0; t < nt; ++t) {
+        for (uint32_t k = 0; k < 3; ++k) {
+            uint32_t g = I[3ull * tris[t] + k];
+            if (vlocal[g] < 0) { if (V >= 256) return OR_ERR_LIMITS; vlocal[g] = (int32_t)V; em->vlist[V++] = g; }
+            em->idx3[3 * t + k] = (uint8_t)vlocal[g];
+        }
+        em->src_tri[t] = tris[t];
+    }
+    for (uint32_t v = 0; v < V; ++v) vlocal[em->vlist[v]] = -1;
+    em->V = V;
+    em->Tp = nt;
+    em->R = 0;
+    em->T = nt;
+    return OR_OK;
+}
 
 static int emit_meshlet(const uint32_t *I, const pending *pm, const int32_t *nbr, emitted *em,
                         int32_t *vlocal /* per source vertex, -1 */) {
@@ -451,7 +512,7 @@ int or_encode(const uint32_t *indices, uint32_t T, const float *attr, uint32_t V
               uint32_t **src_vertex_out, uint32_t **src_tri_out, uint32_t *stats) {
     if (!indices && T) return OR_ERR_ARG;
     if (n < 1 || n > 16 || vmax < 3 || vmax > 256 || tmax < 1 || tmax > 256) return OR_ERR_LIMITS;
-    if (codec != CODEC_GTS && codec != CODEC_REUSE) return OR_ERR_ARG;
+    if (codec != CODEC_GTS && codec != CODEC_REUSE && codec != CODEC_BASIC) return OR_ERR_ARG;
     uint32_t S = 0;
     for (uint32_t c = 0; c < n; ++c) {
         if (bits[c] < 1 || bits[c] > 24) return OR_ERR_LIMITS;
@@ -546,6 +607,16 @@ int or_encode(const uint32_t *indices, uint32_t T, const float *attr, uint32_t V
                 }
             }
             ++meshlets_built;
+            if (codec == CODEC_BASIC) {
+                if (grow((void **)&ems, &cap_em, nem + 1, sizeof(emitted))) goto fail;
+                memset(&ems[nem], 0, sizeof(emitted));
+                rc = emit_basic(indices, mtris, mt, &ems[nem], vlocal);
+                if (rc) goto fail;
+                ems[nem].obj = obj;
+                ++nem;
+                rc = OR_ERR_NOMEM;
+                continue;
+            }
 
             /* ---- stripify: repeatedly start at the lowest-position unvisited triangle and
              * walk to the lowest-position unvisited neighbour (a valid path cover) */
@@ -671,8 +742,9 @@ int or_encode(const uint32_t *indices, uint32_t T, const float *attr, uint32_t V
     if (!rsz) { free(delta); free(origin); free(L); goto fail; }
     uint64_t tot_v = 0, tot_tp = 0, tot_t = 0, tot_r = 0;
     for (uint64_t m = 0; m < nem; ++m) {
-        uint32_t W = (ems[m].Tp + 31) / 32;
-        uint32_t nb = codec == CODEC_GTS ? ems[m].Tp - 1 : (ems[m].Tp - 1) - (ems[m].V - 3);
+        uint32_t W = codec == CODEC_BASIC ? 0 : (ems[m].Tp + 31) / 32;
+        uint32_t nb = codec == CODEC_GTS ? ems[m].Tp - 1
+                      : codec == CODEC_BASIC ? 3 * ems[m].Tp : (ems[m].Tp - 1) - (ems[m].V - 3);
         uint64_t s = W_hdr + 4ull * W * (codec == CODEC_REUSE ? 2 : 1) + ((nb + 3ull) & ~3ull) +
                      4ull * (((uint64_t)ems[m].V * S + 31) / 32);
         rsz[m] = up16(s);
@@ -709,10 +781,12 @@ int or_encode(const uint32_t *indices, uint32_t T, const float *attr, uint32_t V
         wr32(r, (uint32_t)vb); wr32(r + 4, (uint32_t)tb);
         r[8] = (uint8_t)(em->V - 1); r[9] = (uint8_t)(em->Tp - 1);
         wr16(r + 10, (uint16_t)em->obj); wr16(r + 12, (uint16_t)em->R); wr16(r + 14, 0);
-        uint32_t W = (em->Tp + 31) / 32;
+        uint32_t W = codec == CODEC_BASIC ? 0 : (em->Tp + 31) / 32;
         uint8_t *lr = r + W_hdr, *inc = lr + 4 * W, *by = inc + (codec == CODEC_REUSE ? 4 * W : 0);
         uint32_t nb = 0, newmax = 2;
-        for (uint32_t t = 1; t < em->Tp; ++t) {
+        if (codec == CODEC_BASIC)
+            for (nb = 0; nb < 3 * em->Tp; ++nb) by[nb] = em->idx3[nb];
+        for (uint32_t t = 1; t < em->Tp && codec != CODEC_BASIC; ++t) {
             uint32_t w = em->N[t + 2];
             if (em->f[t]) wr32(lr + 4 * (t / 32), rd32(lr + 4 * (t / 32)) | (1u << (t % 32)));
             if (codec == CODEC_GTS) by[nb++] = (uint8_t)w;
@@ -784,7 +858,7 @@ int or_pack(uint32_t codec, uint32_t n, const uint8_t *bits, const uint8_t *sem,
     uint32_t W_hdr = (uint32_t)up16(16u + 4u * n);
     uint64_t rec_total = 0, maxrec = 0, tv = 0, ttp = 0, tt = 0;
     for (uint32_t m = 0; m < M; ++m) {
-        uint32_t W = (Tp[m] + 31) / 32;
+        uint32_t W = codec == CODEC_BASIC ? 0 : (Tp[m] + 31) / 32;
         uint64_t s = up16(W_hdr + 4ull * W * (codec == CODEC_REUSE ? 2 : 1) + ((nbytes[m] + 3ull) & ~3ull) +
                           4ull * (((uint64_t)V[m] * S + 31) / 32));
         rec_total += s;
@@ -814,9 +888,9 @@ int or_pack(uint32_t codec, uint32_t n, const uint8_t *bits, const uint8_t *sem,
         r[8] = (uint8_t)(V[m] - 1); r[9] = (uint8_t)(Tp[m] - 1);
         wr16(r + 10, (uint16_t)obj[m]); wr16(r + 12, (uint16_t)R[m]);
         for (uint32_t c = 0; c < n; ++c) wr32(r + 16 + 4 * c, L[(uint64_t)m * n + c]);
-        uint32_t W = (Tp[m] + 31) / 32;
+        uint32_t W = codec == CODEC_BASIC ? 0 : (Tp[m] + 31) / 32;
         uint8_t *plr = r + W_hdr, *pinc = plr + 4 * W, *pby = pinc + (codec == CODEC_REUSE ? 4 * W : 0);
-        for (uint32_t t = 1; t < Tp[m]; ++t) {
+        for (uint32_t t = 1; t < Tp[m] && codec != CODEC_BASIC; ++t) {
             if (lr[fo + t]) wr32(plr + 4 * (t / 32), rd32(plr + 4 * (t / 32)) | (1u << (t % 32)));
             if (codec == CODEC_REUSE && inc[fo + t])
                 wr32(pinc + 4 * (t / 32), rd32(pinc + 4 * (t / 32)) | (1u << (t % 32)));

@@ -22,13 +22,14 @@ def read_records(blob: np.ndarray):
     for m in range(M):
         r0 = off_rec + 16 * u32(off_dir + 4 * m)
         V, Tp = int(b[r0 + 8]) + 1, int(b[r0 + 9]) + 1
-        W = (Tp + 31) // 32
+        W = 0 if codec == 3 else (Tp + 31) // 32     # Basic records have no flag words
         lr = np.frombuffer(b[r0 + hdr:r0 + hdr + 4 * W].tobytes(), "<u4")
         inc = np.frombuffer(b[r0 + hdr + 4 * W:r0 + hdr + 8 * W].tobytes(), "<u4") if codec == 2 else None
         out.append(dict(vtx_base=u32(r0), tri_base=u32(r0 + 4), V=V, Tp=Tp,
                         object=int(b[r0 + 10]) | (int(b[r0 + 11]) << 8),
                         R=int(b[r0 + 12]) | (int(b[r0 + 13]) << 8),
-                        L=[u32(r0 + 16 + 4 * c) for c in range(n)], lr=lr, inc=inc,
+                        L=[u32(r0 + 16 + 4 * c) for c in range(n)], lr=lr, inc=inc, codec=codec,
+                        basic=(b[r0 + hdr:r0 + hdr + 3 * Tp].copy() if codec == 3 else None),
                         size=16 * (u32(off_dir + 4 * m + 4) - u32(off_dir + 4 * m)), offset=r0, hdr=hdr))
     return out
 
@@ -37,6 +38,12 @@ def gts_meshlet(V, flags, idx):
     """One GTS record's raw fields: flags[t] (t=1..T'-1, 1=R), idx[t-1]."""
     Tp = len(flags) + 1
     return dict(V=V, Tp=Tp, lr=[0] + list(flags), inc=[0] * Tp, bytes=list(idx))
+
+
+def basic_meshlet(V, tris):
+    """One Basic record's raw fields: a local triangle list."""
+    flat = [int(x) for t in tris for x in t]
+    return dict(V=V, Tp=len(tris), lr=[0] * len(tris), inc=[0] * len(tris), bytes=flat)
 
 
 def reuse_meshlet(V, flags, inc, reuse):
