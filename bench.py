@@ -38,6 +38,7 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 METRIC = "decoded triangles/sec (HBM GB/s vs B200 peak in roofline)"
+CODEC_NAMES = {1: "gts", 2: "gts-reuse", 3: "basic"}
 UNIT = "Gtri/s"
 
 WORKLOADS = {
@@ -269,7 +270,7 @@ def run_ours(args, rank, world, local_rank):
     L = blob.layout
     log(f"[rank {rank}] scene built in {time.time() - t0:.1f}s: {L.num_meshlets} meshlets, "
         f"T={L.total_t} T'={L.total_tp} V={L.total_v}, {L.total_bytes / 1e6:.1f} MB")
-    db = mc.DeviceBlob(blob, device=dev, want_vertices=True, want_quantized=False)
+    db = mc.DeviceBlob(blob, device=dev, want_vertices=True, want_quantized=False, index_format=args.index_format)
     stream = torch.cuda.current_stream(dev)
     alg_bytes = db.algorithmic_bytes()
 
@@ -317,25 +318,28 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         data = np.array(blob.bytes)
         h_blob = torch.from_numpy(data).pin_memory()
-        h_idx = torch.empty(3 * L.total_tp, dtype=torch.int32).pin_memory()
+        idx_words = (1 if args.index_format == "u8x4" else 3) * L.total_tp
+        h_idx = torch.empty(idx_words, dtype=torch.int32).pin_memory()
         h_v = torch.empty(L.n_out * L.total_v, dtype=torch.float32).pin_memory()
         ke = max(1, min(args.steps, args.e2e_steps))
         for _ in range(1):
-            mc.mc_decode_host(L, h_blob, db.d_blob, h_idx, db.indices, h_v, db.vertices, stream=stream)
+            mc.mc_decode_host(L, h_blob, db.d_blob, h_idx, db.indices, h_v, db.vertices, flags=db.index_flags,
+                              stream=stream)
         torch.cuda.synchronize(dev)
         if dist:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(ke):
-            mc.mc_decode_host(L, h_blob, db.d_blob, h_idx, db.indices, h_v, db.vertices, stream=stream)
+            mc.mc_decode_host(L, h_blob, db.d_blob, h_idx, db.indices, h_v, db.vertices, flags=db.index_flags,
+                              stream=stream)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if dist:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": tri_all * ke / (float(et[0]) * 1e-3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": int(data.nbytes), "d2h_bytes_per_step": int(12 * L.total_tp + 4 * L.n_out * L.total_v),
+               "h2d_bytes_per_step": int(data.nbytes), "d2h_bytes_per_step": int(4 * idx_words + 4 * L.n_out * L.total_v),
                "steps": ke, "path": "mc_decode_host (pinned host blob -> HBM -> decode -> pinned host outputs)"}
 
     if rank != 0:
@@ -358,7 +362,7 @@ def run_ours(args, rank, world, local_rank):
         "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32/fp32", "data": "synthetic",
         "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
-                   "codec": "gts-reuse" if args.codec == 2 else "gts",
+                   "codec": CODEC_NAMES[args.codec], "index_format": args.index_format,
                    "meshlet": f"{WORKLOADS[args.workload]['vmax']}v/{WORKLOADS[args.workload]['tmax']}t",
                    "triangles_per_gpu": int(tri_local), "decoded_triangles_incl_degenerate_per_gpu": int(L.total_tp),
                    "meshlets_per_gpu": int(L.num_meshlets), "compressed_bytes_per_gpu": int(L.total_bytes),
@@ -386,7 +390,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=list(WORKLOADS), default="cfg4_city")
-    ap.add_argument("--codec", type=int, default=2)
+    ap.add_argument("--codec", type=int, default=2, choices=[1, 2, 3], help="1 GTS, 2 GTS-Reuse, 3 Basic")
+    ap.add_argument("--index-format", default="u32", choices=["u32", "u8x4"],
+                    help="u32: 3 global indices per triangle (default); u8x4: one local u8x4 word")
     ap.add_argument("--instances", type=int, default=1000, help="cfg4 instances per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=10)

@@ -42,7 +42,9 @@ typedef enum {
     MC_ERR_NOMEM = 7     /* host allocation failed                                         */
 } mc_status;
 
-enum { MC_CODEC_GTS = 1, MC_CODEC_GTS_REUSE = 2 };              /* P:420–422 / P:423–426 */
+enum { MC_CODEC_GTS = 1, MC_CODEC_GTS_REUSE = 2,              /* P:420–422 / P:423–426 */
+       MC_CODEC_BASIC = 3 /* 3 local u8 indices per triangle: the paper's Basic mesh-shading
+                             control, 24 bpt (Table 2) */ };
 enum { MC_SEM_GENERIC = 0, MC_SEM_POSITION = 1, MC_SEM_NORMAL = 2, MC_SEM_TEXCOORD = 3,
        MC_SEM_NORMAL_OCT = 4 /* one of two consecutive octahedral channels, FORMAT.md §4.3 */ };
 
@@ -51,8 +53,12 @@ enum { MC_DERR_RECORD = 1, MC_DERR_COUNTS = 2, MC_DERR_INDEX = 4, MC_DERR_REUSE 
 
 /* decode flags */
 enum {
-    MC_DECODE_BLOB_LOCAL_INDICES = 1  /* index value = vtx_base - base_vtx + local (shard-local
+    MC_DECODE_BLOB_LOCAL_INDICES = 1, /* index value = vtx_base - base_vtx + local (shard-local
                                          vertex buffer) instead of the global vtx_base + local */
+    MC_DECODE_INDEX_LOCAL_U8X4 = 2    /* one u32 per triangle, local u8 indices a|b<<8|c<<16
+                                         (FORMAT.md §2; the paper's 8-bit meshlet indices,
+                                         P:294): d_indices then holds total_tp words, 4 B/tri
+                                         instead of 12; a consumer adds the record's vtx_base */
 };
 
 /* ------------------------------------------------------------------ source mesh
@@ -152,7 +158,8 @@ typedef struct {
     const void *d_blob;        /* device: the blob bytes (16-B aligned base)              */
     uint32_t first, count;     /* records [first, first+count) of this blob               */
     uint32_t *d_indices;       /* device, required: 3*total_tp u32, FORMAT.md §2
-                                  (positions relative to base_tri of the blob)            */
+                                  (positions relative to base_tri of the blob); total_tp
+                                  u32 with MC_DECODE_INDEX_LOCAL_U8X4                      */
     float *d_vertices;         /* device or NULL: n_out*total_v fp32, FORMAT.md §4.2       */
     uint32_t *d_quantized;     /* device or NULL: n*total_v u32 grid values, §4.1          */
     uint32_t flags;            /* MC_DECODE_*                                             */
@@ -173,8 +180,11 @@ typedef struct {
     uint32_t num_bad;              /* malformed records                                   */
 } mc_stats;
 
-/* Decode records into the output buffers (the timed hot path).  One warp per
- * meshlet, records staged into shared memory with TMA bulk copies. */
+/* Decode records into the output buffers (the timed hot path).  One 16-lane group
+ * (T~ <= 128) or one warp per meshlet, records staged into shared memory with TMA
+ * bulk copies.  Errors: MC_ERR_ARG (NULL/misaligned pointers, range
+ * outside the blob, unknown flag), MC_ERR_FORMAT (layout not from mc_parse_header),
+ * MC_ERR_LIMITS (staging buffers do not fit shared memory), MC_ERR_CUDA. */
 mc_status mc_decode_meshlets(const mc_decode_args *args, void *stream);
 
 /* Same decode, additionally accumulating mc_stats into *d_stats (device). */

@@ -19,8 +19,8 @@ from . import _build
 
 LIB_PATH = _build.LIB
 
-MC_CODEC_GTS, MC_CODEC_GTS_REUSE = 1, 2
-MC_DECODE_BLOB_LOCAL_INDICES = 1
+MC_CODEC_GTS, MC_CODEC_GTS_REUSE, MC_CODEC_BASIC = 1, 2, 3
+MC_DECODE_BLOB_LOCAL_INDICES, MC_DECODE_INDEX_LOCAL_U8X4 = 1, 2
 MC_DERR_RECORD, MC_DERR_COUNTS, MC_DERR_INDEX, MC_DERR_REUSE, MC_DERR_OBJECT = 1, 2, 4, 8, 16
 
 
@@ -233,9 +233,21 @@ def _stream_handle(stream):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def _check_sizes(layout: mc_layout, d_blob, d_indices, d_vertices, d_quantized, flags: int):
+    """Refuse device buffers smaller than mc.h states (the C ABI takes raw pointers)."""
+    L = layout
+    need = {"d_blob": (d_blob, L.total_bytes, 1),
+            "d_indices": (d_indices, (1 if flags & MC_DECODE_INDEX_LOCAL_U8X4 else 3) * L.total_tp, 4),
+            "d_vertices": (d_vertices, L.n_out * L.total_v, 4), "d_quantized": (d_quantized, L.n * L.total_v, 4)}
+    for name, (t, n, esz) in need.items():
+        if t is not None and t.numel() * t.element_size() < n * esz:
+            raise MCError(f"{name}: {t.numel() * t.element_size()} bytes < {n * esz} required")
+
+
 def mc_decode_meshlets(layout: mc_layout, d_blob, d_indices, d_vertices=None, d_quantized=None, first: int = 0,
                        count: int | None = None, flags: int = 0, stream=None):
     """Enqueue the decode of records [first, first+count) on `stream` (torch stream or None)."""
+    _check_sizes(layout, d_blob, d_indices, d_vertices, d_quantized, flags)
     count = layout.num_meshlets - first if count is None else count
     a = mc_decode_args(ctypes.pointer(layout), d_blob.data_ptr(), first, count, d_indices.data_ptr(),
                        None if d_vertices is None else d_vertices.data_ptr(),
@@ -249,6 +261,7 @@ def mc_stats_reset(d_stats, stream=None):
 
 def mc_decode_stats(layout: mc_layout, d_blob, d_indices, d_stats, d_vertices=None, d_quantized=None, first: int = 0,
                     count: int | None = None, flags: int = 0, stream=None):
+    _check_sizes(layout, d_blob, d_indices, d_vertices, d_quantized, flags)
     count = layout.num_meshlets - first if count is None else count
     a = mc_decode_args(ctypes.pointer(layout), d_blob.data_ptr(), first, count, d_indices.data_ptr(),
                        None if d_vertices is None else d_vertices.data_ptr(),
@@ -277,31 +290,37 @@ def mc_decode_host(layout: mc_layout, h_blob, d_blob, h_indices, d_indices, h_ve
 class DeviceBlob:
     """A blob resident in HBM plus output buffers sized from its layout (torch tensors)."""
 
-    def __init__(self, blob, device="cuda", want_vertices=True, want_quantized=False):
+    def __init__(self, blob, device="cuda", want_vertices=True, want_quantized=False, index_format="u32"):
+        """index_format: "u32" = three global u32 indices per triangle (FORMAT.md §2),
+        "u8x4" = one word of meshlet-local u8 indices per triangle (MC_DECODE_INDEX_LOCAL_U8X4)."""
         import torch
+        if index_format not in ("u32", "u8x4"):
+            raise ValueError(index_format)
         data = blob.bytes if isinstance(blob, Blob) else np.ascontiguousarray(blob, dtype=np.uint8)
         self.layout = parse_header(data)
         L = self.layout
+        self.index_format = index_format
+        self.index_flags = MC_DECODE_INDEX_LOCAL_U8X4 if index_format == "u8x4" else 0
         self.d_blob = torch.from_numpy(np.array(data, copy=True)).to(device)
-        self.indices = torch.empty(3 * L.total_tp, dtype=torch.int32, device=device)
+        self.indices = torch.empty((1 if self.index_flags else 3) * L.total_tp, dtype=torch.int32, device=device)
         self.vertices = torch.empty(L.n_out * L.total_v, dtype=torch.float32, device=device) if want_vertices else None
         self.quantized = torch.empty(L.n * L.total_v, dtype=torch.int32, device=device) if want_quantized else None
         self.stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=device)
 
     def decode(self, stream=None, flags=0, first=0, count=None):
         mc_decode_meshlets(self.layout, self.d_blob, self.indices, self.vertices, self.quantized, first, count,
-                           flags, stream)
+                           flags | self.index_flags, stream)
 
     def decode_stats(self, stream=None, flags=0, first=0, count=None) -> dict:
         mc_stats_reset(self.stats, stream)
         mc_decode_stats(self.layout, self.d_blob, self.indices, self.stats, self.vertices, self.quantized, first,
-                        count, flags, stream)
+                        count, flags | self.index_flags, stream)
         return read_stats(self.stats)
 
     def algorithmic_bytes(self) -> int:
         """Compressed bytes read (directory + records + object table) + decompressed bytes written."""
         L = self.layout
         read = (L.total_bytes - L.off_rec) + 4 * (L.num_meshlets + 1) + 8 * L.n * L.num_objects
-        write = 12 * L.total_tp + (4 * L.n_out * L.total_v if self.vertices is not None else 0) + \
+        write = (4 if self.index_flags else 12) * L.total_tp + (4 * L.n_out * L.total_v if self.vertices is not None else 0) + \
             (4 * L.n * L.total_v if self.quantized is not None else 0)
         return int(read + write)

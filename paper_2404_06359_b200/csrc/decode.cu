@@ -72,6 +72,7 @@ struct Params {
     uint32_t O, vmax, tmax, n, n_out, S, max_rec;
     uint32_t base_vtx, base_tri, total_v, total_tp;
     uint32_t index_sub;        // subtracted from index values (MC_DECODE_BLOB_LOCAL_INDICES)
+    uint32_t u8x4;             // MC_DECODE_INDEX_LOCAL_U8X4: one local u8x4 word per triangle
     uint32_t hdr_words;        // record header words (16 + 4n rounded to 16) / 4
     uint32_t buf_words;        // per-buffer words (max_rec/4 + 4)
     uint32_t vtx_stage_words;  // vmax*n_out + 8 for the generic layout, else 0
@@ -281,8 +282,10 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
         // ---------------- a1: header (FORMAT.md §1.4) + structural validation (§5)
         const uint32_t vtx_base = R[0], tri_base = R[1], w2 = R[2];
         const uint32_t V = (w2 & 0xFFu) + 1u, Tp = ((w2 >> 8) & 0xFFu) + 1u, object = w2 >> 16;
-        const uint32_t W = (Tp + 31u) >> 5;
-        const uint32_t nb = (CODEC == MC_CODEC_GTS) ? (Tp - 1u) : ((V >= 3u && V - 3u <= Tp - 1u) ? (Tp - 1u) - (V - 3u) : 0u);
+        const uint32_t W = CODEC == MC_CODEC_BASIC ? 0u : (Tp + 31u) >> 5;   // Basic: no flag words
+        const uint32_t nb = (CODEC == MC_CODEC_GTS) ? (Tp - 1u)
+                            : (CODEC == MC_CODEC_BASIC) ? 3u * Tp
+                            : ((V >= 3u && V - 3u <= Tp - 1u) ? (Tp - 1u) - (V - 3u) : 0u);
         const uint32_t lr_w = P.hdr_words;
         const uint32_t inc_w = lr_w + W;
         const uint32_t by_w = inc_w + (CODEC == MC_CODEC_GTS_REUSE ? W : 0u);
@@ -293,13 +296,53 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
         else {
             if (V < 3u || V > P.vmax || Tp > P.tmax) err |= MC_DERR_COUNTS;
             if (object >= P.O) err |= MC_DERR_OBJECT;
+            if (CODEC == MC_CODEC_BASIC && (R[3] & 0xFFFFu) != 0u) err |= MC_DERR_COUNTS;   // Basic: R = 0
             if ((uint64_t)tri_base - P.base_tri + Tp > P.total_tp || tri_base < P.base_tri ||
                 (uint64_t)vtx_base - P.base_vtx + V > P.total_v || vtx_base < P.base_vtx)
                 err |= MC_DERR_RECORD;
         }
         const uint8_t* BY = reinterpret_cast<const uint8_t*>(R + by_w);
         const uint32_t* AT = R + at_w;
+        const uint32_t vout = vtx_base - P.index_sub;
+        uint32_t* idst = P.idx + (P.u8x4 ? 1ull : 3ull) * (tri_base - P.base_tri);
+        uint32_t e2 = 0;
+        // a6: store triangle t (FORMAT.md §2): three global u32 indices, or one local u8x4 word
+        auto emit = [&](uint32_t t, uint32_t a0, uint32_t a1, uint32_t a2) {
+            if (P.u8x4) {
+                const uint32_t wd = a0 | (a1 << 8) | (a2 << 16);
+                st_u32(idst + t, wd);
+                if (STATS) ws.cs_idx += mix64((((uint64_t)tri_base + t) << 32) | wd);
+            } else {
+                const uint32_t o0 = vout + a0, o1 = vout + a1, o2 = vout + a2;
+                uint32_t* d = idst + 3u * t;
+                st_u32(d, o0);
+                st_u32(d + 1, o1);
+                st_u32(d + 2, o2);
+                if (STATS) {
+                    const uint64_t kk = 3ull * ((uint64_t)tri_base + t);
+                    ws.cs_idx += mix64((kk << 32) | o0) + mix64(((kk + 1) << 32) | o1) + mix64(((kk + 2) << 32) | o2);
+                }
+            }
+            if (STATS) ws.degen += (a0 == a1 || a1 == a2 || a0 == a2) ? 1u : 0u;
+        };
 
+        if constexpr (CODEC == MC_CODEC_BASIC) {
+            // ---------------- a3-a6 for Basic: the local triangle list itself
+            if (err) {
+                if (STATS && gl == 0) {
+                    atomicOr(&P.stats->error_bits, err);
+                    atomicMin(&P.stats->first_bad_meshlet, m);
+                    atomicAdd(&P.stats->num_bad, 1u);
+                }
+                __syncwarp(gm);
+                continue;
+            }
+            for (uint32_t t = gl; t < Tp; t += G) {
+                const uint32_t a0 = BY[3u * t], a1 = BY[3u * t + 1u], a2 = BY[3u * t + 2u];
+                if (STATS && (a0 >= V || a1 >= V || a2 >= V)) e2 |= MC_DERR_INDEX;
+                emit(t, a0, a1, a2);
+            }
+        } else {
         // ---------------- per-word prefix state, group lanes 0..W-1 hold word `gl` (W <= 8)
         // valid bits of word `gl`: triangles t < T', bit 0 (t = 0) excluded
         uint32_t vm = 0;
@@ -347,10 +390,7 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
 
         // ---------------- a3/a4/a5/a6: topology, one triangle per lane, G per step
         if (gl < 2) Nbuf[gl] = (uint8_t)gl;                                  // N[0], N[1]
-        const uint32_t vout = vtx_base - P.index_sub;
-        uint32_t* idst = P.idx + 3ull * (tri_base - P.base_tri);
         uint32_t carry = 2u;                                                 // N[t+1] for group lane 0
-        uint32_t e2 = 0;
         const uint32_t nsteps = (Tp + G - 1) / G;
         for (uint32_t j = 0; j < nsteps; ++j) {
             const uint32_t t = G * j + gl;
@@ -387,20 +427,14 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
                 const uint32_t npiv = Nbuf[jj + 1];                          // N[j+1], N[0] if none
                 uint32_t a0 = f ? nprev : npiv, a1 = f ? npiv : nprev;       // a5 (FORMAT.md §2)
                 if (t == 0) { a0 = 0u; a1 = 1u; }
-                const uint32_t o0 = vout + a0, o1 = vout + a1, o2 = vout + w;
-                uint32_t* d = idst + 3u * t;                                 // a6
-                st_u32(d, o0);
-                st_u32(d + 1, o1);
-                st_u32(d + 2, o2);
+                emit(t, a0, a1, w);                                          // a6
                 if (STATS) {
-                    const uint64_t kk = 3ull * ((uint64_t)tri_base + t);
-                    ws.cs_idx += mix64((kk << 32) | o0) + mix64(((kk + 1) << 32) | o1) + mix64(((kk + 2) << 32) | o2);
-                    ws.degen += (a0 == a1 || a1 == w || a0 == w) ? 1u : 0u;
                     if (t > 0) ws.max_lb = max(ws.max_lb, (uint32_t)((int)t - jj));
                     if (t > 0 && !x && wj > 0) ws.multi++;
                 }
             }
         }
+        }   // strip codecs
         if (STATS) {
             e2 = __reduce_or_sync(gm, e2);
             if (gl == 0) {
@@ -620,7 +654,9 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     P.base_tri = L.base_tri;
     P.total_v = L.total_v;
     P.total_tp = L.total_tp;
+    if (a->flags & ~(uint32_t)(MC_DECODE_BLOB_LOCAL_INDICES | MC_DECODE_INDEX_LOCAL_U8X4)) return MC_ERR_ARG;
     P.index_sub = (a->flags & MC_DECODE_BLOB_LOCAL_INDICES) ? L.base_vtx : 0u;
+    P.u8x4 = (a->flags & MC_DECODE_INDEX_LOCAL_U8X4) ? 1u : 0u;
     P.hdr_words = ((16u + 4u * L.n + 15u) & ~15u) / 4u;
     P.buf_words = L.max_record_bytes / 4u + 4u;
     P.vtx_stage_words = 0;
@@ -718,6 +754,9 @@ mc_status dispatch_codec(uint32_t codec, bool stats, int lay, bool b16, const Pa
     if (codec == MC_CODEC_GTS)
         return stats ? dispatch_layout<MC_CODEC_GTS, true>(lay, b16, P, smem, s)
                      : dispatch_layout<MC_CODEC_GTS, false>(lay, b16, P, smem, s);
+    if (codec == MC_CODEC_BASIC)
+        return stats ? dispatch_layout<MC_CODEC_BASIC, true>(lay, b16, P, smem, s)
+                     : dispatch_layout<MC_CODEC_BASIC, false>(lay, b16, P, smem, s);
     return stats ? dispatch_layout<MC_CODEC_GTS_REUSE, true>(lay, b16, P, smem, s)
                  : dispatch_layout<MC_CODEC_GTS_REUSE, false>(lay, b16, P, smem, s);
 }
@@ -788,7 +827,8 @@ mc_status mc_decode_host(const mc_host_decode_args* h, void* stream) {
     a.flags = h->flags;
     mc_status rc = launch(&a, nullptr, s);
     if (rc != MC_OK) return rc;
-    if (cudaMemcpyAsync(h->h_indices, h->d_indices, 12ull * L.total_tp, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    const uint64_t idx_bytes = (h->flags & MC_DECODE_INDEX_LOCAL_U8X4) ? 4ull * L.total_tp : 12ull * L.total_tp;
+    if (cudaMemcpyAsync(h->h_indices, h->d_indices, idx_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
         return MC_ERR_CUDA;
     if (h->h_vertices &&
         cudaMemcpyAsync(h->h_vertices, h->d_vertices, 4ull * L.n_out * L.total_v, cudaMemcpyDeviceToHost, s) != cudaSuccess)

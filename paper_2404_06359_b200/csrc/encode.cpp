@@ -66,8 +66,8 @@ void parallel_for(size_t n, unsigned threads, const std::function<void(size_t)>&
 // Record size in bytes for (V, T'), FORMAT.md §1.4.
 inline uint64_t record_bytes(uint32_t codec, uint32_t n, uint32_t S, uint32_t V, uint32_t Tp) {
     uint64_t hdr = round16(16 + 4ull * n);
-    uint32_t W = (Tp + 31) / 32;
-    uint64_t nb = (codec == MC_CODEC_GTS) ? (Tp - 1) : ((Tp - 1) - (V - 3));
+    uint32_t W = codec == MC_CODEC_BASIC ? 0 : (Tp + 31) / 32;   // Basic: no flag words
+    uint64_t nb = (codec == MC_CODEC_GTS) ? (Tp - 1) : (codec == MC_CODEC_BASIC) ? 3ull * Tp : ((Tp - 1) - (V - 3));
     uint64_t topo = 4ull * W * (codec == MC_CODEC_GTS_REUSE ? 2 : 1) + ((nb + 3) & ~uint64_t(3));
     uint64_t attr = 4ull * ((uint64_t(V) * S + 31) / 32);
     return round16(hdr + topo + attr);
@@ -88,6 +88,7 @@ struct Meshlet {
     std::vector<uint8_t> step;            // N[3..T'+1] local indices, size T'-1
     std::vector<uint8_t> flag;            // f_t, t=0..T'-1 (f_0 = 0)
     std::vector<uint32_t> src_tri;        // [T'] (kNone for restart degenerates)
+    std::vector<uint8_t> tri3;            // Basic: local triangle list [3T]
 };
 
 // ---------------------------------------------------------------- mesh-level encoder
@@ -282,6 +283,27 @@ struct Encoder {
         return true;
     }
 
+    // ---- Basic (codec 3): the meshlet's triangles as a local u8 triangle list, vertices
+    // numbered by first appearance; no strips, no restarts
+    bool emit_basic(const std::vector<uint32_t>& tl, uint32_t object, Meshlet& out) {
+        out.object = object;
+        out.Tp = uint32_t(tl.size());
+        out.R = 0;
+        out.local_to_src.clear();
+        out.tri3.resize(3 * tl.size());
+        out.src_tri.assign(tl.begin(), tl.end());
+        for (size_t i = 0; i < tl.size(); ++i)
+            for (int k = 0; k < 3; ++k) {
+                uint32_t g = tri(tl[i])[k];
+                int32_t l = vlocal[g];
+                if (l < 0) { l = int32_t(out.local_to_src.size()); vlocal[g] = l; out.local_to_src.push_back(g); }
+                out.tri3[3 * i + k] = uint8_t(l);
+            }
+        for (uint32_t g : out.local_to_src) vlocal[g] = -1;
+        out.V = uint32_t(out.local_to_src.size());
+        return out.V >= 3 && out.V <= vmax;
+    }
+
     // ---- meshlet building: compact greedy growth (fewest new vertices first, FIFO inside a
     // score class), seeded from the previous meshlet's frontier; then stripify and shrink
     // from the last-added triangle while T' = T + 4R exceeds T~.
@@ -347,6 +369,16 @@ struct Encoder {
                 }
                 if (pick < 0) break;
                 add(uint32_t(pick));
+            }
+            if (codec == MC_CODEC_BASIC) {
+                Meshlet m;
+                if (!emit_basic(tl, object, m)) return MC_ERR_INPUT;
+                out.push_back(std::move(m));
+                frontier.clear();
+                for (int k = 3; k >= 1; --k)
+                    for (size_t j = head[k]; j < bucket[k].size() && frontier.size() < 64; ++j)
+                        if (assign[bucket[k][j]] < 0) frontier.push_back(bucket[k][j]);
+                continue;
             }
             // stripify; shrink until T' fits
             while (true) {
@@ -566,12 +598,16 @@ mc_status serialise(Encoder& E, mc_blob& out) {
         r[8] = uint8_t(me.V - 1); r[9] = uint8_t(me.Tp - 1);
         put16(r + 10, uint16_t(me.object)); put16(r + 12, uint16_t(me.R)); put16(r + 14, 0);
         for (uint32_t c = 0; c < n; ++c) put32(r + 16 + 4 * c, Lq[m * n + c]);
-        const uint32_t W = (me.Tp + 31) / 32;
+        const uint32_t W = codec == MC_CODEC_BASIC ? 0 : (me.Tp + 31) / 32;
         uint32_t* lr = reinterpret_cast<uint32_t*>(r + hdr);
         uint32_t* inc = lr + W;
         uint8_t* by = reinterpret_cast<uint8_t*>(inc + (codec == MC_CODEC_GTS_REUSE ? W : 0));
         uint32_t nb = 0, top = 2;
-        for (uint32_t t = 1; t < me.Tp; ++t) {
+        if (codec == MC_CODEC_BASIC) {
+            std::memcpy(by, me.tri3.data(), me.tri3.size());
+            nb = uint32_t(me.tri3.size());
+        }
+        for (uint32_t t = 1; t < me.Tp && codec != MC_CODEC_BASIC; ++t) {
             if (me.flag[t]) lr[t / 32] |= 1u << (t % 32);
             uint32_t w = me.step[t - 1];
             if (codec == MC_CODEC_GTS) by[nb++] = uint8_t(w);
@@ -612,7 +648,7 @@ mc_status parse(const uint8_t* b, size_t nbytes, mc_layout* L) {
     L->off_dir = get64(b + 64); L->off_obj = get64(b + 72); L->off_rec = get64(b + 80); L->total_bytes = get64(b + 88);
     std::memcpy(L->bits, b + 96, 16);
     std::memcpy(L->semantic, b + 112, 16);
-    if (L->codec != MC_CODEC_GTS && L->codec != MC_CODEC_GTS_REUSE) return MC_ERR_FORMAT;
+    if (L->codec != MC_CODEC_GTS && L->codec != MC_CODEC_GTS_REUSE && L->codec != MC_CODEC_BASIC) return MC_ERR_FORMAT;
     if (L->n < 1 || L->n > 16 || L->num_objects < 1 || L->v_max < 3 || L->v_max > 256 || L->t_max < 1 ||
         L->t_max > 256)
         return MC_ERR_FORMAT;
@@ -667,7 +703,7 @@ mc_status mc_encode(const mc_mesh* mesh, const mc_encode_params* p, mc_blob** ou
     if (n < 1 || n > 16 || p->max_vertices < 3 || p->max_vertices > 256 || p->max_triangles < 1 ||
         p->max_triangles > 256)
         return MC_ERR_LIMITS;
-    if (p->codec != MC_CODEC_GTS && p->codec != MC_CODEC_GTS_REUSE) return MC_ERR_ARG;
+    if (p->codec != MC_CODEC_GTS && p->codec != MC_CODEC_GTS_REUSE && p->codec != MC_CODEC_BASIC) return MC_ERR_ARG;
     for (uint32_t c = 0; c < n; ++c) {
         if (mesh->bits[c] < 1 || mesh->bits[c] > 24) return MC_ERR_LIMITS;
         if (mesh->semantic[c] > MC_SEM_NORMAL_OCT) return MC_ERR_ARG;

@@ -62,7 +62,7 @@ def test_product_encoder_roundtrip_via_oracle(mc, orc):
     for mesh, lim in [(synth.quad_grid(), (64, 126)), (synth.displaced_sphere(16), (128, 256)),
                       (synth.random_patch(7), (32, 32)), (synth.torus(50, 30), (256, 256)),
                       (synth.random_patch(8), (16, 8))]:
-        for codec in (1, 2):
+        for codec in (1, 2, 3):
             b = mc.mc_encode(mesh, *lim, codec)
             err, errs, idx, q, f = orc.decode(np.array(b.bytes))
             assert err == 0
@@ -73,6 +73,8 @@ def test_product_encoder_roundtrip_via_oracle(mc, orc):
             assert np.array_equal(synth.canonical_triangles(g[~deg]), synth.canonical_triangles(mesh.indices))
             assert deg.sum() == 4 * b.encode_stats()["restarts"]
             assert np.all((st == 0xFFFFFFFF) == deg)
+            if codec == 3:   # Basic: no restarts, T' = T
+                assert b.encode_stats()["restarts"] == 0 and b.layout.total_tp == len(mesh.indices)
             L = b.layout
             assert L.v_max == lim[0] and L.t_max == lim[1]
             from streams import read_records
