@@ -54,7 +54,7 @@ def lib():
         L.or_checksum.argtypes = [P, u64, u64]
         L.or_checksum.restype = u64
         L.or_oct_decode.argtypes = [ctypes.c_float, ctypes.c_float, P]
-        L.or_encode.argtypes = [P, u32, P, u32, u32, P, P, P, u32, u32, u32,
+        L.or_encode.argtypes = [P, u32, P, u32, u32, P, P, P, u32, u32, u32, u32,
                                 ctypes.POINTER(P), ctypes.POINTER(u64), ctypes.POINTER(P),
                                 ctypes.POINTER(P), P]
         L.or_pack.argtypes = [u32, u32, P, P, u32, P, P, u32, u32, u32, P, P, P, P, P, P, P, P, P, P,
@@ -78,7 +78,7 @@ def blob_info(blob: np.ndarray) -> Info:
     if st:
         raise ValueError(f"bad blob (status {st})")
     keys = ["codec", "n", "M", "O", "vmax", "tmax", "total_v", "total_tp", "total_t",
-            "base_meshlet", "base_vtx", "base_tri", "max_record_bytes", "S", "n_out"]
+            "base_meshlet", "base_vtx", "base_tri", "max_record_bytes", "S", "n_out", "vw"]
     return Info({k: int(v) for k, v in zip(keys, out)})
 
 
@@ -93,8 +93,8 @@ class Encoded:
                               [int(x) for x in stats[:7]]))
 
 
-def encode(mesh, vmax: int = 64, tmax: int = 126, codec: int = CODEC_REUSE) -> Encoded:
-    """Oracle encoder (oracle.c ``or_encode``)."""
+def encode(mesh, vmax: int = 64, tmax: int = 126, codec: int = CODEC_REUSE, vw: bool = False) -> Encoded:
+    """Oracle encoder (oracle.c ``or_encode``); ``vw``: per-meshlet attribute widths (FORMAT.md §1.4)."""
     idx = np.ascontiguousarray(mesh.indices, dtype=np.uint32).reshape(-1)
     attr = np.ascontiguousarray(mesh.attributes, dtype=np.float32)
     bits = np.asarray(mesh.bits, np.uint8)
@@ -103,7 +103,7 @@ def encode(mesh, vmax: int = 64, tmax: int = 126, codec: int = CODEC_REUSE) -> E
     bp, bn, sv, st = ctypes.c_void_p(), ctypes.c_uint64(), ctypes.c_void_p(), ctypes.c_void_p()
     stats = np.zeros(8, np.uint32)
     rc = lib().or_encode(_p(idx), mesh.num_triangles, _p(attr), mesh.num_vertices, mesh.n, _p(bits), _p(sem),
-                         _p(obj), vmax, tmax, codec, ctypes.byref(bp), ctypes.byref(bn), ctypes.byref(sv),
+                         _p(obj), vmax, tmax, codec, 1 if vw else 0, ctypes.byref(bp), ctypes.byref(bn), ctypes.byref(sv),
                          ctypes.byref(st), _p(stats))
     if rc:
         raise ValueError(f"oracle encode failed: status {rc}")

@@ -18,6 +18,8 @@
  *     P:459-467) and the crack-free global-grid quantiser.
  *   - Basic (codec 3): the paper's uncompressed mesh-shading control — three
  *     local u8 indices per triangle (Table 2).
+ *   - VW blobs (FORMAT.md §1.4, extension f1): per-meshlet attribute widths
+ *     w_c = bit length of the meshlet's largest code on the unchanged global grid.
  *   - or_pack: serialises caller-given raw streams WITHOUT validation so tests
  *     can build exhaustive and malformed inputs.
  * Floating point: compiled with -ffp-contract=off; every fused multiply-add is an
@@ -96,6 +98,7 @@ typedef struct {
     uint64_t off_dir, off_obj, off_rec, total_bytes;
     uint8_t bits[16], sem[16];
     uint32_t S, n_out;
+    uint32_t vw;   /* FORMAT.md §1.1 flags bit 0: per-meshlet attribute widths (extension f1) */
 } or_hdr;
 
 static int parse_header(const uint8_t *b, size_t nbytes, or_hdr *h) {
@@ -108,6 +111,9 @@ static int parse_header(const uint8_t *b, size_t nbytes, or_hdr *h) {
     h->total_bytes = rd64(b + 88);
     memcpy(h->bits, b + 96, 16);
     memcpy(h->sem, b + 112, 16);
+    uint32_t flags = rd32(b + 60);
+    if (flags & ~1u) return OR_ERR_FORMAT;
+    h->vw = flags & 1u;
     if (h->codec != CODEC_GTS && h->codec != CODEC_REUSE && h->codec != CODEC_BASIC) return OR_ERR_FORMAT;
     if (h->n < 1 || h->n > 16 || h->O < 1) return OR_ERR_FORMAT;
     if (h->total_bytes != nbytes) return OR_ERR_FORMAT;
@@ -134,7 +140,7 @@ int or_blob_info(const uint8_t *blob, size_t nbytes, uint32_t *out /* 16 u32 */)
     int st = parse_header(blob, nbytes, &h);
     if (st) return st;
     uint32_t v[16] = {h.codec, h.n, h.M, h.O, h.vmax, h.tmax, h.total_v, h.total_tp, h.total_t,
-                      h.base_meshlet, h.base_vtx, h.base_tri, h.max_record_bytes, h.S, h.n_out, 0};
+                      h.base_meshlet, h.base_vtx, h.base_tri, h.max_record_bytes, h.S, h.n_out, h.vw};
     memcpy(out, v, sizeof v);
     return OR_OK;
 }
@@ -188,7 +194,15 @@ uint32_t or_decode_meshlet(const uint8_t *blob, size_t nbytes, uint32_t m, uint3
     uint32_t n = h.n;
     /* Basic records have no flag words (FORMAT.md §1.4) */
     uint32_t W = h.codec == CODEC_BASIC ? 0u : (Tp + 31u) / 32u;
-    uint64_t hdr_bytes = up16(16u + 4ull * n);
+    uint64_t hdr_bytes = up16(16u + 4ull * n + (h.vw ? n : 0u));
+    /* attribute widths: the blob's b_c, or the record's w_c with VW (FORMAT.md §1.4) */
+    uint8_t wid[16];
+    uint32_t S = 0, wbad = 0;
+    for (uint32_t c = 0; c < n; ++c) {
+        wid[c] = h.vw ? rec[16 + 4 * n + c] : h.bits[c];
+        if (wid[c] > h.bits[c]) wbad = 1;
+        S += wid[c];
+    }
     uint32_t nb;
     if (h.codec == CODEC_GTS) nb = Tp - 1u;
     else if (h.codec == CODEC_BASIC) nb = 3u * Tp;
@@ -197,10 +211,10 @@ uint32_t or_decode_meshlet(const uint8_t *blob, size_t nbytes, uint32_t m, uint3
     uint64_t off_inc = off_lr + 4ull * W;
     uint64_t off_bytes = off_inc + (h.codec == CODEC_REUSE ? 4ull * W : 0ull);
     uint64_t off_attr = off_bytes + ((nb + 3ull) & ~3ull);
-    uint64_t attr_words = ((uint64_t)V * h.S + 31u) / 32u;
+    uint64_t attr_words = ((uint64_t)V * S + 31u) / 32u;
     uint64_t size = up16(off_attr + 4ull * attr_words);
     uint32_t err = 0;
-    if (size != r1 - r0 || size > h.max_record_bytes) return DERR_RECORD;
+    if (size != r1 - r0 || size > h.max_record_bytes || wbad) return DERR_RECORD;
     if (V < 3u || V > h.vmax || Tp > h.tmax) err |= DERR_COUNTS;
     if (object >= h.O) err |= DERR_OBJECT;
     if (h.codec == CODEC_BASIC && R != 0u) err |= DERR_COUNTS;   /* Basic has no restarts */
@@ -265,11 +279,11 @@ attributes:
     if ((q_out || f_out) && !(err & (DERR_OBJECT | DERR_COUNTS))) {
         const uint8_t *obj = blob + h.off_obj + 8ull * n * object;
         for (uint32_t v = 0; v < V; ++v) {
-            uint64_t p = (uint64_t)v * h.S;
+            uint64_t p = (uint64_t)v * S;
             uint32_t q[16];
             for (uint32_t ch = 0; ch < n; ++ch) {
-                uint32_t code = get_field(AT, p, h.bits[ch]);
-                p += h.bits[ch];
+                uint32_t code = get_field(AT, p, wid[ch]);
+                p += wid[ch];
                 q[ch] = rd32(rec + 16 + 4 * ch) + code;
                 if (q_out) q_out[(uint64_t)v * n + ch] = q[ch];
             }
@@ -508,7 +522,7 @@ static int emit_meshlet(const uint32_t *I, const pending *pm, const int32_t *nbr
  * stats[8] = {M, total_V, total_Tp, total_T, restarts, meshlets_before_split, O, 0}. */
 int or_encode(const uint32_t *indices, uint32_t T, const float *attr, uint32_t Vsrc, uint32_t n,
               const uint8_t *bits, const uint8_t *sem, const uint32_t *obj_of_tri, uint32_t vmax,
-              uint32_t tmax, uint32_t codec, uint8_t **blob_out, uint64_t *blob_bytes,
+              uint32_t tmax, uint32_t codec, uint32_t vw, uint8_t **blob_out, uint64_t *blob_bytes,
               uint32_t **src_vertex_out, uint32_t **src_tri_out, uint32_t *stats) {
     if (!indices && T) return OR_ERR_ARG;
     if (n < 1 || n > 16 || vmax < 3 || vmax > 256 || tmax < 1 || tmax > 256) return OR_ERR_LIMITS;
@@ -735,37 +749,61 @@ int or_encode(const uint32_t *indices, uint32_t T, const float *attr, uint32_t V
             origin[(uint64_t)obj * n + ch] = g;
         }
 
+    /* ---- per-meshlet L_c (lowest grid value) and, with VW, the code width
+     * w_c = bit length of the largest code Q - L_c (FORMAT.md §1.4, extension f1) */
+    uint8_t *wid = malloc((nem ? nem : 1) * n);
+    if (!wid) { free(delta); free(origin); free(L); goto fail; }
+    for (uint64_t m = 0; m < nem; ++m) {
+        const emitted *em = &ems[m];
+        const float *dl = delta + (uint64_t)em->obj * n, *og = origin + (uint64_t)em->obj * n;
+        for (uint32_t ch = 0; ch < n; ++ch) {
+            double qlo = INFINITY, qhi = -INFINITY;
+            for (uint32_t v = 0; v < em->V; ++v) {
+                double Q = floor(((double)attr[(uint64_t)em->vlist[v] * n + ch] - (double)og[ch]) / (double)dl[ch] + 0.5);
+                if (Q < qlo) qlo = Q;
+                if (Q > qhi) qhi = Q;
+            }
+            L[m * n + ch] = (uint32_t)qlo;
+            uint32_t maxcode = (uint32_t)(qhi - qlo), w = 0;
+            while (w < 32 && (maxcode >> w) != 0) ++w;     /* bit length */
+            wid[m * n + ch] = vw ? (uint8_t)w : bits[ch];
+        }
+    }
+
     /* ---- serialise (FORMAT.md §1) */
-    uint32_t W_hdr = (uint32_t)up16(16u + 4u * n);
+    uint32_t W_hdr = (uint32_t)up16(16u + 4u * n + (vw ? n : 0u));
     uint64_t rec_total = 0, maxrec = 0;
     uint64_t *rsz = malloc(sizeof(uint64_t) * (nem ? nem : 1));
-    if (!rsz) { free(delta); free(origin); free(L); goto fail; }
+    if (!rsz) { free(wid); free(delta); free(origin); free(L); goto fail; }
     uint64_t tot_v = 0, tot_tp = 0, tot_t = 0, tot_r = 0;
     for (uint64_t m = 0; m < nem; ++m) {
+        uint32_t Sm = 0;
+        for (uint32_t ch = 0; ch < n; ++ch) Sm += wid[m * n + ch];
         uint32_t W = codec == CODEC_BASIC ? 0 : (ems[m].Tp + 31) / 32;
         uint32_t nb = codec == CODEC_GTS ? ems[m].Tp - 1
                       : codec == CODEC_BASIC ? 3 * ems[m].Tp : (ems[m].Tp - 1) - (ems[m].V - 3);
         uint64_t s = W_hdr + 4ull * W * (codec == CODEC_REUSE ? 2 : 1) + ((nb + 3ull) & ~3ull) +
-                     4ull * (((uint64_t)ems[m].V * S + 31) / 32);
+                     4ull * (((uint64_t)ems[m].V * Sm + 31) / 32);
         rsz[m] = up16(s);
         rec_total += rsz[m];
         if (rsz[m] > maxrec) maxrec = rsz[m];
         tot_v += ems[m].V; tot_tp += ems[m].Tp; tot_t += ems[m].T; tot_r += ems[m].R;
     }
     if (tot_v > 0xFFFFFFFFull || 3 * tot_tp > 0xFFFFFFFFull || rec_total / 16 > 0xFFFFFFFFull) {
-        rc = OR_ERR_RANGE; free(rsz); free(delta); free(origin); free(L); goto fail;
+        rc = OR_ERR_RANGE; free(wid); free(rsz); free(delta); free(origin); free(L); goto fail;
     }
     uint64_t off_dir = 160, off_obj = up16(off_dir + 4ull * (nem + 1)), off_rec = up16(off_obj + 8ull * n * O);
     uint64_t total = off_rec + rec_total;
     uint8_t *B = calloc(total, 1);
     uint32_t *srcv = malloc(sizeof(uint32_t) * (tot_v ? tot_v : 1));
     uint32_t *srct = malloc(sizeof(uint32_t) * (tot_tp ? tot_tp : 1));
-    if (!B || !srcv || !srct) { free(B); free(srcv); free(srct); free(rsz); free(delta); free(origin); free(L); goto fail; }
+    if (!B || !srcv || !srct) { free(B); free(srcv); free(srct); free(wid); free(rsz); free(delta); free(origin); free(L); goto fail; }
     memcpy(B, "MCZ1", 4);
     wr32(B + 4, 1); wr32(B + 8, codec); wr32(B + 12, n); wr32(B + 16, (uint32_t)nem); wr32(B + 20, O);
     wr32(B + 24, vmax); wr32(B + 28, tmax); wr32(B + 32, (uint32_t)tot_v); wr32(B + 36, (uint32_t)tot_tp);
     wr32(B + 40, (uint32_t)tot_t); wr32(B + 44, 0); wr32(B + 48, 0); wr32(B + 52, 0);
     wr32(B + 56, (uint32_t)maxrec);
+    wr32(B + 60, vw ? 1u : 0u);
     wr64(B + 64, off_dir); wr64(B + 72, off_obj); wr64(B + 80, off_rec); wr64(B + 88, total);
     for (uint32_t c = 0; c < n; ++c) { B[96 + c] = bits[c]; B[112 + c] = sem[c]; }
     for (uint32_t o = 0; o < O; ++o)
@@ -795,21 +833,18 @@ int or_encode(const uint32_t *indices, uint32_t T, const float *attr, uint32_t V
         }
         uint8_t *at = by + ((nb + 3u) & ~3u);
         const float *dl = delta + (uint64_t)em->obj * n, *og = origin + (uint64_t)em->obj * n;
+        uint32_t Sm = 0;
         for (uint32_t ch = 0; ch < n; ++ch) {
-            double qlo = INFINITY;
-            for (uint32_t v = 0; v < em->V; ++v) {
-                double Q = floor(((double)attr[(uint64_t)em->vlist[v] * n + ch] - (double)og[ch]) / (double)dl[ch] + 0.5);
-                if (Q < qlo) qlo = Q;
-            }
-            wr32(r + 16 + 4 * ch, (uint32_t)qlo);
-            L[m * n + ch] = (uint32_t)qlo;
+            wr32(r + 16 + 4 * ch, L[m * n + ch]);
+            if (vw) r[16 + 4 * n + ch] = wid[m * n + ch];
+            Sm += wid[m * n + ch];
         }
         for (uint32_t v = 0; v < em->V; ++v) {
-            uint64_t p = (uint64_t)v * S;
+            uint64_t p = (uint64_t)v * Sm;
             for (uint32_t ch = 0; ch < n; ++ch) {
                 double Q = floor(((double)attr[(uint64_t)em->vlist[v] * n + ch] - (double)og[ch]) / (double)dl[ch] + 0.5);
                 uint32_t code = (uint32_t)Q - L[m * n + ch];
-                for (unsigned k = 0; k < bits[ch]; ++k, ++p)
+                for (unsigned k = 0; k < wid[m * n + ch]; ++k, ++p)
                     if ((code >> k) & 1u) wr32(at + 4 * (p / 32), rd32(at + 4 * (p / 32)) | (1u << (p % 32)));
             }
             srcv[vb + v] = em->vlist[v];
@@ -829,7 +864,7 @@ int or_encode(const uint32_t *indices, uint32_t T, const float *attr, uint32_t V
     *blob_bytes = total;
     if (src_vertex_out) *src_vertex_out = srcv; else free(srcv);
     if (src_tri_out) *src_tri_out = srct; else free(srct);
-    free(rsz); free(delta); free(origin); free(L);
+    free(wid); free(rsz); free(delta); free(origin); free(L);
     rc = OR_OK;
 fail:
     free(nbr); free(ems); free(assigned); free(vstamp); free(vlocal); free(mtris); free(queue);

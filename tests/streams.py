@@ -16,8 +16,9 @@ def read_records(blob: np.ndarray):
     u32 = lambda off: int(np.frombuffer(b[off:off + 4].tobytes(), "<u4")[0])
     u64 = lambda off: int(np.frombuffer(b[off:off + 8].tobytes(), "<u8")[0])
     codec, n, M = u32(8), u32(12), u32(16)
+    vw = u32(60) & 1                                   # per-meshlet widths (FORMAT.md §1.4)
     off_dir, off_rec = u64(64), u64(80)
-    hdr = (16 + 4 * n + 15) // 16 * 16
+    hdr = (16 + 4 * n + (n if vw else 0) + 15) // 16 * 16
     out = []
     for m in range(M):
         r0 = off_rec + 16 * u32(off_dir + 4 * m)
@@ -30,6 +31,8 @@ def read_records(blob: np.ndarray):
                         R=int(b[r0 + 12]) | (int(b[r0 + 13]) << 8),
                         L=[u32(r0 + 16 + 4 * c) for c in range(n)], lr=lr, inc=inc, codec=codec,
                         basic=(b[r0 + hdr:r0 + hdr + 3 * Tp].copy() if codec == 3 else None),
+                        widths=([int(x) for x in b[r0 + 16 + 4 * n:r0 + 16 + 5 * n]] if vw
+                                else [int(x) for x in b[96:96 + n]]),
                         size=16 * (u32(off_dir + 4 * m + 4) - u32(off_dir + 4 * m)), offset=r0, hdr=hdr))
     return out
 
