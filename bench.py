@@ -56,12 +56,13 @@ def log(*a):
 
 # ----------------------------------------------------------------------------- scenes
 
-def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: int, protos_k=(16, 91)):
+def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: int, protos_k=(16, 91),
+               vw: bool = False):
     """The rank's shard of the workload as a product-encoded blob (mc_encode path)."""
     w = WORKLOADS[workload]
     if workload == "cfg4_city":
         scene = synth.city(num_instances=instances * world, num_prototypes=protos_k[0], k=protos_k[1], seed=0)
-        protos = [mc.mc_encode(p, w["vmax"], w["tmax"], codec) for p in scene.prototypes]
+        protos = [mc.mc_encode(p, w["vmax"], w["tmax"], codec, variable_widths=vw) for p in scene.prototypes]
         blob = mc.mc_blob_instance_range(protos, scene.instance_proto, scene.instance_offset,
                                          rank * instances, instances)
         meta = {"instances_per_gpu": instances, "prototypes": protos_k[0],
@@ -71,7 +72,7 @@ def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: 
     mesh = {"cfg1_grid": lambda: synth.quad_grid(32, 32),
             "cfg2_torus": lambda: synth.torus(1000, 500),
             "cfg3_sphere": lambda: synth.displaced_sphere(913)}[workload]()
-    blob = mc.mc_encode(mesh, w["vmax"], w["tmax"], codec)
+    blob = mc.mc_encode(mesh, w["vmax"], w["tmax"], codec, variable_widths=vw)
     meta = {"restarts_per_meshlet": round(blob.encode_stats()["restarts"] / max(1, blob.layout.num_meshlets), 3)}
     if world > 1:   # strong-sharded replicas of the single mesh
         f, c = blob.shard_ranges(world)[rank]
@@ -230,7 +231,7 @@ def run_reference(args, rank, world):
     import oracle
     oracle.build()
     import paper_2404_06359_b200 as mc
-    blob, meta = build_blob(mc, args.workload, 0, 1, args.codec, args.instances)
+    blob, meta = build_blob(mc, args.workload, 0, 1, args.codec, args.instances, vw=args.variable_widths)
     data = np.array(blob.bytes)
     cores = host_cores()
     per_step = max(0.5, min(3.0, 150.0 / max(1, args.steps + args.warmup)))
@@ -266,7 +267,7 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     t0 = time.time()
-    blob, meta = build_blob(mc, args.workload, rank, world, args.codec, args.instances)
+    blob, meta = build_blob(mc, args.workload, rank, world, args.codec, args.instances, vw=args.variable_widths)
     L = blob.layout
     log(f"[rank {rank}] scene built in {time.time() - t0:.1f}s: {L.num_meshlets} meshlets, "
         f"T={L.total_t} T'={L.total_tp} V={L.total_v}, {L.total_bytes / 1e6:.1f} MB")
@@ -363,6 +364,8 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "u32/fp32", "data": "synthetic",
         "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
                    "codec": CODEC_NAMES[args.codec], "index_format": args.index_format,
+                   "attribute_widths": "per-meshlet (VW)" if args.variable_widths else "global b",
+                   "compressed_bits_per_tri": round(8.0 * L.total_bytes / max(1, L.total_t), 3),
                    "meshlet": f"{WORKLOADS[args.workload]['vmax']}v/{WORKLOADS[args.workload]['tmax']}t",
                    "triangles_per_gpu": int(tri_local), "decoded_triangles_incl_degenerate_per_gpu": int(L.total_tp),
                    "meshlets_per_gpu": int(L.num_meshlets), "compressed_bytes_per_gpu": int(L.total_bytes),
@@ -391,6 +394,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=list(WORKLOADS), default="cfg4_city")
     ap.add_argument("--codec", type=int, default=2, choices=[1, 2, 3], help="1 GTS, 2 GTS-Reuse, 3 Basic")
+    ap.add_argument("--variable-widths", action="store_true",
+                    help="per-meshlet attribute code widths (FORMAT.md VW, extension f1)")
     ap.add_argument("--index-format", default="u32", choices=["u32", "u8x4"],
                     help="u32: 3 global indices per triangle (default); u8x4: one local u8x4 word")
     ap.add_argument("--instances", type=int, default=1000, help="cfg4 instances per GPU")

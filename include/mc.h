@@ -78,11 +78,18 @@ typedef struct {
                                             cross objects                             */
 } mc_mesh;
 
+enum {
+    MC_ENCODE_VARIABLE_WIDTHS = 1   /* per-meshlet attribute code widths w_c = bit length of the
+                                       meshlet's largest code on the unchanged global grid
+                                       (FORMAT.md §1.4 VW, motivated by P:715–716) */
+};
+
 typedef struct {
     uint32_t max_vertices;   /* Ṽ (the paper uses 128)                          */
     uint32_t max_triangles;  /* T̃, bounds T' = T + 4R (the paper uses 256)       */
     uint32_t codec;          /* MC_CODEC_*                                              */
     uint32_t num_threads;    /* host worker threads, 0 = hardware concurrency           */
+    uint32_t flags;          /* MC_ENCODE_*                                             */
 } mc_encode_params;
 
 typedef struct mc_blob mc_blob;   /* opaque, library-owned, immutable host object */
@@ -94,7 +101,8 @@ typedef struct {
     uint32_t total_v, total_tp, total_t;  /* Σ V, Σ T' (decoded), Σ T (real)             */
     uint32_t base_meshlet, base_vtx, base_tri, max_record_bytes;
     uint64_t off_dir, off_obj, off_rec, total_bytes;
-    uint8_t bits[16], semantic[16];
+    uint8_t bits[16], semantic[16];   /* global grid widths b_c and semantics          */
+    uint32_t flags;                   /* BlobHeader flags (bit 0 VW: per-record widths) */
 } mc_layout;
 
 /* Encode a mesh (P:279–305 meshlets; P:312–467 strips; P:486–492 quantisation).
@@ -211,7 +219,7 @@ typedef struct {
 mc_status mc_decode_host(const mc_host_decode_args *args, void *stream);
 
 const char *mc_status_str(mc_status s);
-uint32_t mc_abi_version(void);   /* 1 */
+uint32_t mc_abi_version(void);   /* 2 (mc_encode_params.flags, mc_layout.flags) */
 
 #ifdef __cplusplus
 }

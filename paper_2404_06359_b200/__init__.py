@@ -21,6 +21,8 @@ LIB_PATH = _build.LIB
 
 MC_CODEC_GTS, MC_CODEC_GTS_REUSE, MC_CODEC_BASIC = 1, 2, 3
 MC_DECODE_BLOB_LOCAL_INDICES, MC_DECODE_INDEX_LOCAL_U8X4 = 1, 2
+MC_ENCODE_VARIABLE_WIDTHS = 1
+ABI_VERSION = 2
 MC_DERR_RECORD, MC_DERR_COUNTS, MC_DERR_INDEX, MC_DERR_REUSE, MC_DERR_OBJECT = 1, 2, 4, 8, 16
 
 
@@ -33,7 +35,8 @@ class mc_layout(ctypes.Structure):
                 ("codec", "n", "n_out", "S", "num_meshlets", "num_objects", "v_max", "t_max",
                  "total_v", "total_tp", "total_t", "base_meshlet", "base_vtx", "base_tri", "max_record_bytes")] + \
                [("off_dir", ctypes.c_uint64), ("off_obj", ctypes.c_uint64), ("off_rec", ctypes.c_uint64),
-                ("total_bytes", ctypes.c_uint64), ("bits", ctypes.c_uint8 * 16), ("semantic", ctypes.c_uint8 * 16)]
+                ("total_bytes", ctypes.c_uint64), ("bits", ctypes.c_uint8 * 16), ("semantic", ctypes.c_uint8 * 16),
+                ("flags", ctypes.c_uint32)]
 
 
 class mc_mesh(ctypes.Structure):
@@ -45,7 +48,7 @@ class mc_mesh(ctypes.Structure):
 
 class mc_encode_params(ctypes.Structure):
     _fields_ = [("max_vertices", ctypes.c_uint32), ("max_triangles", ctypes.c_uint32),
-                ("codec", ctypes.c_uint32), ("num_threads", ctypes.c_uint32)]
+                ("codec", ctypes.c_uint32), ("num_threads", ctypes.c_uint32), ("flags", ctypes.c_uint32)]
 
 
 class mc_decode_args(ctypes.Structure):
@@ -90,6 +93,8 @@ def lib() -> ctypes.CDLL:
             getattr(L, name).restype = ctypes.c_int
         L.mc_status_str.restype = ctypes.c_char_p
         L.mc_abi_version.restype = u32
+        if L.mc_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH}: ABI {L.mc_abi_version()} != {ABI_VERSION}; rebuild with __graft_entry__.build()")
         L.mc_encode.argtypes = [ctypes.POINTER(mc_mesh), ctypes.POINTER(mc_encode_params), ctypes.POINTER(P)]
         L.mc_blob_instance.argtypes = [P, u32, P, P, u32, ctypes.POINTER(P)]
         L.mc_blob_instance_range.argtypes = [P, u32, P, P, u32, u32, u32, ctypes.POINTER(P)]
@@ -122,21 +127,37 @@ def _p(a):
 
 # ----------------------------------------------------------------------------- blobs
 
+class _Handle:
+    """Owns one mc_blob; freed when the last Blob or byte view referencing it dies."""
+
+    def __init__(self, h: ctypes.c_void_p):
+        self.h = h
+
+    def __del__(self):
+        if self.h is not None and _lib is not None:
+            _lib.mc_blob_free(self.h)
+            self.h = None
+
+
+class _View:
+    """numpy __array_interface__ over the blob's bytes that keeps its _Handle alive."""
+
+    def __init__(self, handle: _Handle, ptr: int, n: int):
+        self.handle = handle
+        self.__array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, True), "version": 3}
+
+
 class Blob:
     """An encoded meshlet stream (FORMAT.md) owned by libmc (``mc_blob``)."""
 
     def __init__(self, handle: ctypes.c_void_p):
+        self._owner = _Handle(handle)
         self._h = handle
         bp, n = ctypes.c_void_p(), ctypes.c_size_t()
         _check(lib().mc_blob_bytes(self._h, ctypes.byref(bp), ctypes.byref(n)), "mc_blob_bytes")
-        self.bytes = np.ctypeslib.as_array(ctypes.cast(bp, ctypes.POINTER(ctypes.c_uint8)), (n.value,))
+        # read-only view; it keeps the library object alive even after this Blob is gone
+        self.bytes = np.asarray(_View(self._owner, bp.value or 0, n.value))
         self.layout = parse_header(self.bytes)
-
-    def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and _lib is not None:
-            _lib.mc_blob_free(h)
-            self._h = None
 
     @classmethod
     def from_bytes(cls, data: np.ndarray) -> "Blob":
@@ -172,8 +193,9 @@ def parse_header(data: np.ndarray) -> mc_layout:
 
 
 def mc_encode(mesh, max_vertices: int = 64, max_triangles: int = 126, codec: int = MC_CODEC_GTS_REUSE,
-              num_threads: int = 0) -> Blob:
-    """Encode a mesh (any object with indices/attributes/bits/semantic[/object_of_triangle])."""
+              num_threads: int = 0, variable_widths: bool = False) -> Blob:
+    """Encode a mesh (any object with indices/attributes/bits/semantic[/object_of_triangle]);
+    ``variable_widths``: per-meshlet attribute code widths (MC_ENCODE_VARIABLE_WIDTHS)."""
     idx = np.ascontiguousarray(mesh.indices, dtype=np.uint32)
     attr = np.ascontiguousarray(mesh.attributes, dtype=np.float32)
     bits = np.ascontiguousarray(np.asarray(mesh.bits, dtype=np.uint8))
@@ -182,7 +204,8 @@ def mc_encode(mesh, max_vertices: int = 64, max_triangles: int = 126, codec: int
     obj = None if obj is None else np.ascontiguousarray(obj, dtype=np.uint32)
     m = mc_mesh(attr.shape[0], idx.reshape(-1, 3).shape[0], _p(idx), _p(attr), attr.shape[1], _p(bits), _p(sem),
                 _p(obj))
-    prm = mc_encode_params(max_vertices, max_triangles, codec, num_threads)
+    prm = mc_encode_params(max_vertices, max_triangles, codec, num_threads,
+                           MC_ENCODE_VARIABLE_WIDTHS if variable_widths else 0)
     h = ctypes.c_void_p()
     _check(lib().mc_encode(ctypes.byref(m), ctypes.byref(prm), ctypes.byref(h)), "mc_encode")
     return Blob(h)

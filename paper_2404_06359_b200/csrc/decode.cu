@@ -73,7 +73,8 @@ struct Params {
     uint32_t base_vtx, base_tri, total_v, total_tp;
     uint32_t index_sub;        // subtracted from index values (MC_DECODE_BLOB_LOCAL_INDICES)
     uint32_t u8x4;             // MC_DECODE_INDEX_LOCAL_U8X4: one local u8x4 word per triangle
-    uint32_t hdr_words;        // record header words (16 + 4n rounded to 16) / 4
+    uint32_t hdr_words;        // record header words (16 + 4n [+ n with VW] rounded to 16) / 4
+    uint32_t vw;               // FORMAT.md VW: per-record attribute widths w_c after L_c
     uint32_t buf_words;        // per-buffer words (max_rec/4 + 4)
     uint32_t vtx_stage_words;  // vmax*n_out + 8 for the generic layout, else 0
     uint32_t grp_words;        // smem words per group: 2 buffers + vertex stage + misc, padded
@@ -194,12 +195,15 @@ struct WarpStats {
 // half-warp an independent "group" with its own staging buffers, barriers and lane
 // masks; halves the per-meshlet uniform work (header, scans, staging) per warp).
 // NCH > 0: compile-time channel count (register arrays, static indexing), OCT0 = first
-// channel of the octahedral pair or -1; B16: every channel is 16 bits wide (the paper's
+// channel of the octahedral pair or -1; AM (attribute mode): 0 = every channel 16 bits
+// wide, read as aligned halfwords; 1 = bit reader with the blob's widths; 2 = bit reader
+// with each record's widths (FORMAT.md VW).  B16 (AM == 0): every channel is 16 bits wide (the paper's
 // b = 16) so codes are read as aligned halfwords.  NCH == 0: generic
 // runtime layout (any n <= 16, widths 1..24, any octahedral placement).
-template <int G, int CODEC, bool STATS, int NCH, int OCT0, bool B16>
+template <int G, int CODEC, bool STATS, int NCH, int OCT0, int AM>
 __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(const __grid_constant__ Params P) {
     static_assert(G == 8 || G == 16 || G == 32, "group size");
+    constexpr bool B16 = AM == 0, VWK = AM == 2;
     constexpr int NG = 32 / G;                      // groups (meshlets in flight) per warp
     constexpr int NOUT = NCH > 0 ? NCH + (OCT0 >= 0 ? 1 : 0) : 1;
     const uint32_t n_out = NCH > 0 ? (uint32_t)NOUT : P.n_out;
@@ -290,9 +294,20 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
         const uint32_t inc_w = lr_w + W;
         const uint32_t by_w = inc_w + (CODEC == MC_CODEC_GTS_REUSE ? W : 0u);
         const uint32_t at_w = by_w + ((nb + 3u) >> 2);
-        const uint32_t need = ((at_w + ((V * P.S + 31u) >> 5)) * 4u + 15u) & ~15u;
+        // attribute widths: the blob's b_c, or this record's w_c <= b_c with VW (FORMAT.md §1.4)
+        const uint8_t* WB = reinterpret_cast<const uint8_t*>(R) + 16u + 4u * P.n;
+        uint32_t Sm = P.S, wbad = 0;
+        if constexpr (VWK) {
+            Sm = 0;
+            for (uint32_t c = 0; c < P.n; ++c) {
+                const uint32_t w = WB[c];
+                wbad |= w > P.bits[c] ? 1u : 0u;
+                Sm += w;
+            }
+        }
+        const uint32_t need = ((at_w + ((V * Sm + 31u) >> 5)) * 4u + 15u) & ~15u;
         uint32_t err = 0;
-        if (staged == 0 || need != staged) err |= MC_DERR_RECORD;
+        if (staged == 0 || need != staged || wbad) err |= MC_DERR_RECORD;
         else {
             if (V < 3u || V > P.vmax || Tp > P.tmax) err |= MC_DERR_COUNTS;
             if (object >= P.O) err |= MC_DERR_OBJECT;
@@ -472,8 +487,12 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
                         og[c] = __ldg(ot + NCH + c);
                     }
                 }
+                uint32_t bw[NCH];                                            // code widths
 #pragma unroll
-                for (int c = 0; c < NCH; ++c) Lc[c] = R[4 + c];
+                for (int c = 0; c < NCH; ++c) {
+                    Lc[c] = R[4 + c];
+                    bw[c] = B16 ? 16u : (VWK ? (uint32_t)WB[c] : (uint32_t)P.bits[c]);
+                }
                 for (uint32_t v = gl; v < V; v += G) {
                     uint32_t qv[NCH];
                     if constexpr (B16) {
@@ -482,14 +501,14 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
                         for (int c = 0; c < NCH; ++c) qv[c] = Lc[c] + H[c];   // q = L_c + code
                     } else {
                         // little-endian bit reader over the vertex record (FORMAT.md §1.4)
-                        const uint32_t bit0 = v * P.S;
+                        const uint32_t bit0 = v * Sm;
                         const uint32_t* wp = AT + (bit0 >> 5);
                         uint64_t acc = (uint64_t)(wp[0] >> (bit0 & 31u));
                         uint32_t avail = 32u - (bit0 & 31u);
                         ++wp;
 #pragma unroll
                         for (int c = 0; c < NCH; ++c) {
-                            const uint32_t bb = P.bits[c];
+                            const uint32_t bb = bw[c];
                             if (avail < bb) { acc |= (uint64_t)(*wp++) << avail; avail += 32u; }
                             qv[c] = Lc[c] + ((uint32_t)acc & ((1u << bb) - 1u));
                             acc >>= bb;
@@ -542,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
                 const uint32_t fphase = want_f ? ((uint32_t)(reinterpret_cast<uintptr_t>(fdst) >> 2) & 3u) : 0u;
                 uint32_t* vst = vtx_stage + fphase;
                 for (uint32_t v = gl; v < V; v += G) {
-                    const uint32_t bit0 = v * P.S;
+                    const uint32_t bit0 = v * Sm;
                     const uint32_t* wp = AT + (bit0 >> 5);
                     uint64_t acc = (uint64_t)(wp[0] >> (bit0 & 31u));
                     uint32_t avail = 32u - (bit0 & 31u);
@@ -550,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
                     uint32_t* qd = want_q ? P.qout + (size_t)P.n * (vpos + v) : nullptr;
                     float xprev = 0.0f;
                     for (uint32_t c = 0; c < P.n; ++c) {
-                        const uint32_t bb = P.bits[c];
+                        const uint32_t bb = VWK ? (uint32_t)WB[c] : (uint32_t)P.bits[c];
                         if (avail < bb) { acc |= (uint64_t)(*wp++) << avail; avail += 32u; }
                         const uint32_t q = R[4 + c] + ((uint32_t)acc & ((1u << bb) - 1u));
                         acc >>= bb;
@@ -657,7 +676,8 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     if (a->flags & ~(uint32_t)(MC_DECODE_BLOB_LOCAL_INDICES | MC_DECODE_INDEX_LOCAL_U8X4)) return MC_ERR_ARG;
     P.index_sub = (a->flags & MC_DECODE_BLOB_LOCAL_INDICES) ? L.base_vtx : 0u;
     P.u8x4 = (a->flags & MC_DECODE_INDEX_LOCAL_U8X4) ? 1u : 0u;
-    P.hdr_words = ((16u + 4u * L.n + 15u) & ~15u) / 4u;
+    P.vw = L.flags & 1u;
+    P.hdr_words = ((16u + 4u * L.n + (P.vw ? L.n : 0u) + 15u) & ~15u) / 4u;
     P.buf_words = L.max_record_bytes / 4u + 4u;
     P.vtx_stage_words = 0;
     P.idx = a->d_indices;
@@ -687,9 +707,9 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     return MC_OK;
 }
 
-template <int G, int CODEC, bool STATS, int NCH, int OCT0, bool B16>
+template <int G, int CODEC, bool STATS, int NCH, int OCT0, int AM>
 mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
-    auto kern = mc_decode_kernel<G, CODEC, STATS, NCH, OCT0, B16>;
+    auto kern = mc_decode_kernel<G, CODEC, STATS, NCH, OCT0, AM>;
     constexpr uint32_t NG = 32 / G;
     const size_t warp_smem = NG * grp_smem;
     // warps per CTA: 8, fewer when a warp's staging buffers are large (Ṽ=T̃=256, 24-bit)
@@ -731,34 +751,42 @@ mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
 
 // group size: two meshlets per warp (G = 16) when a meshlet has at most
 // MC_GROUP16_TMAX decoded triangles, else one meshlet per warp (G = 32)
-template <int CODEC, bool STATS, int NCH, int OCT0, bool B16>
+template <int CODEC, bool STATS, int NCH, int OCT0, int AM>
 mc_status launch_t(const Params& P, size_t grp_smem, cudaStream_t s) {
 #if MC_GROUP8
-    if (P.tmax <= MC_GROUP16_TMAX) return launch_g<8, CODEC, STATS, NCH, OCT0, B16>(P, grp_smem, s);
+    if (P.tmax <= MC_GROUP16_TMAX) return launch_g<8, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
 #endif
-    if (P.tmax <= MC_GROUP16_TMAX) return launch_g<16, CODEC, STATS, NCH, OCT0, B16>(P, grp_smem, s);
-    return launch_g<32, CODEC, STATS, NCH, OCT0, B16>(P, grp_smem, s);
+    if (P.tmax <= MC_GROUP16_TMAX) return launch_g<16, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
+    return launch_g<32, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
+}
+
+template <int CODEC, bool STATS, int NCH, int OCT0>
+mc_status dispatch_am(int am, const Params& P, size_t smem, cudaStream_t s) {
+    if constexpr (NCH > 0)
+        if (am == 0) return launch_t<CODEC, STATS, NCH, OCT0, 0>(P, smem, s);
+    if (am == 2) return launch_t<CODEC, STATS, NCH, OCT0, 2>(P, smem, s);
+    return launch_t<CODEC, STATS, NCH, OCT0, 1>(P, smem, s);
 }
 
 template <int CODEC, bool STATS>
-mc_status dispatch_layout(int lay, bool b16, const Params& P, size_t smem, cudaStream_t s) {
+mc_status dispatch_layout(int lay, int am, const Params& P, size_t smem, cudaStream_t s) {
     switch (lay) {
-        case 1: return b16 ? launch_t<CODEC, STATS, 8, -1, true>(P, smem, s) : launch_t<CODEC, STATS, 8, -1, false>(P, smem, s);
-        case 2: return b16 ? launch_t<CODEC, STATS, 7, 3, true>(P, smem, s) : launch_t<CODEC, STATS, 7, 3, false>(P, smem, s);
-        case 3: return b16 ? launch_t<CODEC, STATS, 3, -1, true>(P, smem, s) : launch_t<CODEC, STATS, 3, -1, false>(P, smem, s);
-        default: return launch_t<CODEC, STATS, 0, -1, false>(P, smem, s);
+        case 1: return dispatch_am<CODEC, STATS, 8, -1>(am, P, smem, s);
+        case 2: return dispatch_am<CODEC, STATS, 7, 3>(am, P, smem, s);
+        case 3: return dispatch_am<CODEC, STATS, 3, -1>(am, P, smem, s);
+        default: return dispatch_am<CODEC, STATS, 0, -1>(am, P, smem, s);
     }
 }
 
-mc_status dispatch_codec(uint32_t codec, bool stats, int lay, bool b16, const Params& P, size_t smem, cudaStream_t s) {
+mc_status dispatch_codec(uint32_t codec, bool stats, int lay, int am, const Params& P, size_t smem, cudaStream_t s) {
     if (codec == MC_CODEC_GTS)
-        return stats ? dispatch_layout<MC_CODEC_GTS, true>(lay, b16, P, smem, s)
-                     : dispatch_layout<MC_CODEC_GTS, false>(lay, b16, P, smem, s);
+        return stats ? dispatch_layout<MC_CODEC_GTS, true>(lay, am, P, smem, s)
+                     : dispatch_layout<MC_CODEC_GTS, false>(lay, am, P, smem, s);
     if (codec == MC_CODEC_BASIC)
-        return stats ? dispatch_layout<MC_CODEC_BASIC, true>(lay, b16, P, smem, s)
-                     : dispatch_layout<MC_CODEC_BASIC, false>(lay, b16, P, smem, s);
-    return stats ? dispatch_layout<MC_CODEC_GTS_REUSE, true>(lay, b16, P, smem, s)
-                 : dispatch_layout<MC_CODEC_GTS_REUSE, false>(lay, b16, P, smem, s);
+        return stats ? dispatch_layout<MC_CODEC_BASIC, true>(lay, am, P, smem, s)
+                     : dispatch_layout<MC_CODEC_BASIC, false>(lay, am, P, smem, s);
+    return stats ? dispatch_layout<MC_CODEC_GTS_REUSE, true>(lay, am, P, smem, s)
+                 : dispatch_layout<MC_CODEC_GTS_REUSE, false>(lay, am, P, smem, s);
 }
 
 mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s) {
@@ -777,8 +805,10 @@ mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s) {
     if (L.n == 8 && noct == 0) lay = 1;                   // pos3 + nrm3 + uv2
     else if (L.n == 7 && noct == 1 && oct0 == 3) lay = 2; // pos3 + oct2 + uv2 (cfg3/cfg4)
     else if (L.n == 3 && noct == 0) lay = 3;              // positions only (cfg2)
+    // attribute mode: 0 aligned halfwords (every channel 16 bits, no VW), 1 bit reader, 2 VW
     bool b16 = true;
     for (uint32_t c = 0; c < L.n; ++c) b16 = b16 && L.bits[c] == 16;
+    const int am = (L.flags & 1u) ? 2 : (b16 ? 0 : 1);
     if (lay == 0)   // generic kernel stages vertex words in smem
         P.vtx_stage_words = a->d_vertices ? ((L.v_max * L.n_out + 8u + 3u) & ~3u) : 0u;
     // group stride = 16 (mod 32) words: the two groups of a warp reading the same
@@ -786,7 +816,7 @@ mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s) {
     P.grp_words = 2 * P.buf_words + P.vtx_stage_words + kMiscWords;
     if (MC_BANK_PAD) P.grp_words += (48u - (P.grp_words & 31u)) & 31u;
     smem = 4u * (size_t)P.grp_words;
-    return dispatch_codec(L.codec, st != nullptr, lay, b16, P, smem, s);
+    return dispatch_codec(L.codec, st != nullptr, lay, am, P, smem, s);
 }
 
 }  // namespace

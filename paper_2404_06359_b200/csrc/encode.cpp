@@ -64,8 +64,8 @@ void parallel_for(size_t n, unsigned threads, const std::function<void(size_t)>&
 }
 
 // Record size in bytes for (V, T'), FORMAT.md §1.4.
-inline uint64_t record_bytes(uint32_t codec, uint32_t n, uint32_t S, uint32_t V, uint32_t Tp) {
-    uint64_t hdr = round16(16 + 4ull * n);
+inline uint64_t record_bytes(uint32_t codec, uint32_t n, uint32_t S, uint32_t V, uint32_t Tp, bool vw = false) {
+    uint64_t hdr = round16(16 + 4ull * n + (vw ? n : 0));   // VW: + u8 w_c[n]
     uint32_t W = codec == MC_CODEC_BASIC ? 0 : (Tp + 31) / 32;   // Basic: no flag words
     uint64_t nb = (codec == MC_CODEC_GTS) ? (Tp - 1) : (codec == MC_CODEC_BASIC) ? 3ull * Tp : ((Tp - 1) - (V - 3));
     uint64_t topo = 4ull * W * (codec == MC_CODEC_GTS_REUSE ? 2 : 1) + ((nb + 3) & ~uint64_t(3));
@@ -104,8 +104,9 @@ struct Encoder {
     std::vector<uint16_t> tpos;          // scratch: triangle -> position in its meshlet
     std::vector<int32_t> vlocal;         // scratch: vertex -> local index during emission
 
-    Encoder(const mc_mesh& m, uint32_t vm, uint32_t tm, uint32_t cd, unsigned th)
-        : mesh(m), vmax(vm), tmax(tm), codec(cd), threads(th), n(m.num_channels), S(0) {
+    bool vw = false;                     // MC_ENCODE_VARIABLE_WIDTHS
+    Encoder(const mc_mesh& m, uint32_t vm, uint32_t tm, uint32_t cd, unsigned th, bool varw = false)
+        : mesh(m), vmax(vm), tmax(tm), codec(cd), threads(th), n(m.num_channels), S(0), vw(varw) {
         for (uint32_t c = 0; c < n; ++c) S += m.bits[c];
     }
 
@@ -485,12 +486,12 @@ namespace {
 void write_header(uint8_t* B, uint32_t codec, uint32_t n, uint32_t M, uint32_t O, uint32_t vmax,
                   uint32_t tmax, uint64_t tv, uint64_t ttp, uint64_t tt, uint32_t base_m, uint32_t base_v,
                   uint32_t base_t, uint32_t maxrec, uint64_t off_dir, uint64_t off_obj, uint64_t off_rec,
-                  uint64_t total, const uint8_t* bits, const uint8_t* sem) {
+                  uint64_t total, const uint8_t* bits, const uint8_t* sem, uint32_t flags = 0) {
     std::memcpy(B, "MCZ1", 4);
     put32(B + 4, 1); put32(B + 8, codec); put32(B + 12, n); put32(B + 16, M); put32(B + 20, O);
     put32(B + 24, vmax); put32(B + 28, tmax); put32(B + 32, uint32_t(tv)); put32(B + 36, uint32_t(ttp));
     put32(B + 40, uint32_t(tt)); put32(B + 44, base_m); put32(B + 48, base_v); put32(B + 52, base_t);
-    put32(B + 56, maxrec); put32(B + 60, 0);
+    put32(B + 56, maxrec); put32(B + 60, flags);
     put64(B + 64, off_dir); put64(B + 72, off_obj); put64(B + 80, off_rec); put64(B + 88, total);
     std::memset(B + 96, 0, 64);
     for (uint32_t c = 0; c < n; ++c) { B[96 + c] = bits[c]; B[112 + c] = sem[c]; }
@@ -499,7 +500,7 @@ void write_header(uint8_t* B, uint32_t codec, uint32_t n, uint32_t M, uint32_t O
 // Quantise and serialise (FORMAT.md §1, §3).
 mc_status serialise(Encoder& E, mc_blob& out) {
     const mc_mesh& mesh = E.mesh;
-    const uint32_t n = E.n, S = E.S, O = E.num_objects, codec = E.codec;
+    const uint32_t n = E.n, O = E.num_objects, codec = E.codec;
     auto& ms = E.meshlets;
     const size_t M = ms.size();
     const unsigned th = E.threads;
@@ -530,6 +531,8 @@ mc_status serialise(Encoder& E, mc_blob& out) {
             wmax[k] = std::max(wmax[k], double(mhi[m * n + c]) - double(mlo[m * n + c]));
         }
     std::vector<uint32_t> Lq(M * n);
+    std::vector<uint8_t> wq(M * n);    // per-meshlet code widths (VW) or the global b_c
+    const bool vw = E.vw;
     auto qof = [](float x, float g, float d) { return std::floor((double(x) - double(g)) / double(d) + 0.5); };
     for (uint32_t o = 0; o < O; ++o)
         for (uint32_t c = 0; c < n; ++c) {
@@ -554,6 +557,10 @@ mc_status serialise(Encoder& E, mc_blob& out) {
                 double hi = qof(mhi[m * n + c], origin[k], delta[k]);
                 if (hi > 4294967295.0) range_err = 1;
                 Lq[m * n + c] = uint32_t(lo);
+                // Q is monotone in the attribute, so the largest code is Q(max) - Q(min)
+                uint32_t mc = hi - lo > 0 ? uint32_t(hi - lo) : 0u, w = 0;
+                while (w < 32 && (mc >> w)) ++w;
+                wq[m * n + c] = vw ? uint8_t(w) : mesh.bits[c];
                 if (hi - lo > double((1u << mesh.bits[c]) - 1u)) bad[k] = 1;
             }
         });
@@ -568,7 +575,9 @@ mc_status serialise(Encoder& E, mc_blob& out) {
     uint64_t tv = 0, ttp = 0, tt = 0, maxrec = 0, rs = 0;
     std::vector<uint32_t> vb(M), tb(M);
     for (size_t m = 0; m < M; ++m) {
-        uint64_t sz = record_bytes(codec, n, S, ms[m].V, ms[m].Tp);
+        uint32_t Sm = 0;
+        for (uint32_t c = 0; c < n; ++c) Sm += wq[m * n + c];
+        uint64_t sz = record_bytes(codec, n, Sm, ms[m].V, ms[m].Tp, vw);
         roff[m + 1] = roff[m] + sz;
         maxrec = std::max(maxrec, sz);
         vb[m] = uint32_t(tv);
@@ -581,7 +590,7 @@ mc_status serialise(Encoder& E, mc_blob& out) {
     if (!out.allocate(total)) return MC_ERR_NOMEM;
     uint8_t* B = out.bytes;
     write_header(B, codec, n, uint32_t(M), O, E.vmax, E.tmax, tv, ttp, tt, 0, 0, 0, uint32_t(maxrec), off_dir,
-                 off_obj, off_rec, total, mesh.bits, mesh.semantic);
+                 off_obj, off_rec, total, mesh.bits, mesh.semantic, vw ? 1u : 0u);
     for (size_t m = 0; m <= M; ++m) put32(B + off_dir + 4 * m, uint32_t(roff[m] / 16));
     for (uint32_t o = 0; o < O; ++o)
         for (uint32_t c = 0; c < n; ++c) {
@@ -590,7 +599,7 @@ mc_status serialise(Encoder& E, mc_blob& out) {
         }
     out.src_vertex.resize(tv);
     out.src_tri.resize(ttp);
-    const uint64_t hdr = round16(16 + 4ull * n);
+    const uint64_t hdr = round16(16 + 4ull * n + (vw ? n : 0));
     parallel_for(M, th, [&](size_t m) {
         const Meshlet& me = ms[m];
         uint8_t* r = B + off_rec + roff[m];
@@ -598,6 +607,8 @@ mc_status serialise(Encoder& E, mc_blob& out) {
         r[8] = uint8_t(me.V - 1); r[9] = uint8_t(me.Tp - 1);
         put16(r + 10, uint16_t(me.object)); put16(r + 12, uint16_t(me.R)); put16(r + 14, 0);
         for (uint32_t c = 0; c < n; ++c) put32(r + 16 + 4 * c, Lq[m * n + c]);
+        if (vw)
+            for (uint32_t c = 0; c < n; ++c) r[16 + 4 * n + c] = wq[m * n + c];
         const uint32_t W = codec == MC_CODEC_BASIC ? 0 : (me.Tp + 31) / 32;
         uint32_t* lr = reinterpret_cast<uint32_t*>(r + hdr);
         uint32_t* inc = lr + W;
@@ -621,7 +632,8 @@ mc_status serialise(Encoder& E, mc_blob& out) {
             const float* A = mesh.attributes + uint64_t(me.local_to_src[v]) * n;
             for (uint32_t c = 0; c < n; ++c) {
                 uint32_t code = uint32_t(qof(A[c], origin[ob + c], delta[ob + c])) - Lq[m * n + c];
-                uint32_t b = mesh.bits[c];
+                uint32_t b = wq[m * n + c];
+                if (b == 0) continue;
                 uint64_t word = bitpos >> 5, sh = bitpos & 31;
                 at[word] |= code << sh;
                 if (sh + b > 32) at[word + 1] |= code >> (32 - sh);
@@ -648,6 +660,8 @@ mc_status parse(const uint8_t* b, size_t nbytes, mc_layout* L) {
     L->off_dir = get64(b + 64); L->off_obj = get64(b + 72); L->off_rec = get64(b + 80); L->total_bytes = get64(b + 88);
     std::memcpy(L->bits, b + 96, 16);
     std::memcpy(L->semantic, b + 112, 16);
+    L->flags = get32(b + 60);
+    if (L->flags & ~1u) return MC_ERR_FORMAT;
     if (L->codec != MC_CODEC_GTS && L->codec != MC_CODEC_GTS_REUSE && L->codec != MC_CODEC_BASIC) return MC_ERR_FORMAT;
     if (L->n < 1 || L->n > 16 || L->num_objects < 1 || L->v_max < 3 || L->v_max > 256 || L->t_max < 1 ||
         L->t_max > 256)
@@ -678,7 +692,7 @@ mc_status parse(const uint8_t* b, size_t nbytes, mc_layout* L) {
 // ================================================================= C ABI (host part)
 extern "C" {
 
-uint32_t mc_abi_version(void) { return 1; }
+uint32_t mc_abi_version(void) { return 2; }
 
 const char* mc_status_str(mc_status s) {
     switch (s) {
@@ -719,7 +733,8 @@ mc_status mc_encode(const mc_mesh* mesh, const mc_encode_params* p, mc_blob** ou
         if (v[0] == v[1] || v[1] == v[2] || v[0] == v[2]) return MC_ERR_INPUT;
     }
     try {
-        Encoder E(*mesh, p->max_vertices, p->max_triangles, p->codec, worker_count(p->num_threads));
+        Encoder E(*mesh, p->max_vertices, p->max_triangles, p->codec, worker_count(p->num_threads),
+                  (p->flags & MC_ENCODE_VARIABLE_WIDTHS) != 0);
         mc_status st = E.run();
         if (st != MC_OK) return st;
         auto blob = std::make_unique<mc_blob>();
@@ -826,7 +841,8 @@ mc_status mc_blob_extract(const void* bytes, size_t n, uint32_t first, uint32_t 
         maxrec = std::max<uint64_t>(maxrec, r1 - r0);
     }
     write_header(B, L.codec, L.n, count, L.num_objects, L.v_max, L.t_max, tv, ttp, tt, L.base_meshlet + first, bv, bt,
-                 uint32_t(std::max<uint64_t>(maxrec, 16)), off_dir, off_obj, off_rec, total, L.bits, L.semantic);
+                 uint32_t(std::max<uint64_t>(maxrec, 16)), off_dir, off_obj, off_rec, total, L.bits, L.semantic,
+                 L.flags);
     for (uint32_t m = 0; m <= count; ++m) put32(B + off_dir + 4ull * m, uint32_t(get32(b + L.off_dir + 4ull * (first + m)) - d0));
     std::memcpy(B + off_obj, b + L.off_obj, 8ull * L.n * L.num_objects);
     std::memcpy(B + off_rec, b + L.off_rec + 16 * d0, rec_bytes);
@@ -851,6 +867,7 @@ mc_status mc_blob_instance_range(const mc_blob* const* protos, uint32_t num_prot
         mc_status st = parse(protos[p]->bytes, protos[p]->size, &Ls[p]);
         if (st != MC_OK) return st;
         if (Ls[p].codec != Ls[0].codec || Ls[p].n != Ls[0].n || std::memcmp(Ls[p].bits, Ls[0].bits, 16) ||
+            Ls[p].flags != Ls[0].flags ||
             std::memcmp(Ls[p].semantic, Ls[0].semantic, 16))
             return MC_ERR_ARG;
     }
@@ -887,7 +904,7 @@ mc_status mc_blob_instance_range(const mc_blob* const* protos, uint32_t num_prot
     if (!blob->allocate(total)) return MC_ERR_NOMEM;
     uint8_t* B = blob->bytes;
     write_header(B, L0.codec, n, uint32_t(M), uint32_t(O), vmax, tmax, tv, ttp, tt, uint32_t(gm), uint32_t(gv),
-                 uint32_t(gt), uint32_t(maxrec), off_dir, off_obj, off_rec, total, L0.bits, L0.semantic);
+                 uint32_t(gt), uint32_t(maxrec), off_dir, off_obj, off_rec, total, L0.bits, L0.semantic, L0.flags);
     // per-instance prefix sums, then fill instances in parallel
     std::vector<uint64_t> im(num_instances + 1, 0), io(num_instances + 1, 0), iv(num_instances + 1, 0),
         it(num_instances + 1, 0), ir(num_instances + 1, 0);

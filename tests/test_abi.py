@@ -29,7 +29,7 @@ def test_exports_every_declared_symbol(mc):
     L = mc.lib()
     for name in sorted(declared):
         assert hasattr(L, name), name
-    assert L.mc_abi_version() == 1
+    assert L.mc_abi_version() == 2
     out = os.popen(f"nm -D {mc.LIB_PATH}").read()
     for name in declared:
         assert re.search(rf"\bT {name}\b", out), name
@@ -136,3 +136,25 @@ def test_instance_range_shards(mc, orc):
                                       fe[4].view(np.uint32)[L.n_out * L.base_vtx:L.n_out * (L.base_vtx + L.total_v)])
         cs = (cs + orc.checksum(idx, 3 * L.base_tri)) % 2**64
     assert cs == orc.checksum(fe[2], 0)
+
+
+@pytest.mark.parametrize("codec", [1, 2, 3])
+def test_product_encoder_variable_widths(mc, orc, codec):
+    """mc_encode(variable_widths=True) (FORMAT.md VW): the oracle decodes it to exactly the
+    values of the fixed-width product blob, and each record's w_c is the bit length of
+    its largest code (brute force over the decoded meshlet)."""
+    from streams import read_records
+    for mesh in (synth.displaced_sphere(20), synth.random_patch(6), synth.torus(40, 20).with_bits(13)):
+        fixed = np.array(mc.mc_encode(mesh, 64, 126, codec).bytes)
+        var = np.array(mc.mc_encode(mesh, 64, 126, codec, variable_widths=True).bytes)
+        assert mc.parse_header(var).flags == 1 and mc.parse_header(fixed).flags == 0
+        a, b = orc.decode(fixed), orc.decode(var)
+        assert a[0] == 0 and b[0] == 0
+        assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
+        assert np.array_equal(a[4].view(np.uint32), b[4].view(np.uint32))
+        n = orc.blob_info(var).n
+        q = b[3].reshape(-1, n).astype(np.int64)
+        for r in read_records(var):
+            codes = q[r["vtx_base"]:r["vtx_base"] + r["V"]] - np.array(r["L"], np.int64)
+            for c in range(n):
+                assert int(codes[:, c].max()).bit_length() == r["widths"][c] <= mesh.bits[c]
