@@ -154,8 +154,9 @@ struct Encoder {
         }, 4096);
     }
 
-    // ---- greedy path cover of one meshlet's dual graph: start at a minimum-degree
-    // triangle, extend both ends to the minimum-degree unvisited neighbour.
+    // ---- path cover of one meshlet's dual graph (maximise strip edges under
+    // degree <= 2 and no cycles): a greedy cover (start at a minimum-degree triangle,
+    // extend both ends to the minimum-degree unvisited neighbour), then tunnelling.
     // Returns strips as lists of positions into `tl`.
     void stripify(const std::vector<uint32_t>& tl, const std::vector<int32_t>& assign, int32_t id,
                   std::vector<std::vector<uint16_t>>& strips) {
@@ -203,6 +204,120 @@ struct Encoder {
                     --left;
                 }
                 std::reverse(path.begin(), path.end());
+            }
+            strips.push_back(std::move(path));
+        }
+        if (tunnel_budget) tunnel(ln, T, strips);
+    }
+
+    // ---- strip-count reduction by tunnelling (the idea of the Enhanced Tunneling
+    // Algorithm the paper compares against): a tunnel is an alternating path
+    // free-edge, strip-edge, ..., free-edge between two strip terminals (triangles with
+    // fewer than two strip neighbours).  Flipping it adds one strip edge, so the number of
+    // strips (and restarts) drops by one, provided no cycle forms (every
+    // dual-graph path is a valid generalized strip).  Breadth-first search per
+    // terminal, bounded depth; a flip that closes a cycle is undone.
+    unsigned tunnel_budget = 512;   // flips tried per meshlet
+    void tunnel(const std::vector<int16_t>& ln, uint32_t T, std::vector<std::vector<uint16_t>>& strips) {
+        if (strips.size() < 2) return;
+        std::vector<int16_t> sn(2 * T, -1);                      // strip neighbours
+        auto has = [&](int u, int v) { return sn[2 * u] == v || sn[2 * u + 1] == v; };
+        auto deg = [&](int u) { return int(sn[2 * u] >= 0) + int(sn[2 * u + 1] >= 0); };
+        auto add = [&](int u, int v) { (sn[2 * u] < 0 ? sn[2 * u] : sn[2 * u + 1]) = int16_t(v); };
+        auto del = [&](int u, int v) { (sn[2 * u] == v ? sn[2 * u] : sn[2 * u + 1]) = -1; };
+        for (auto& p : strips)
+            for (size_t i = 1; i < p.size(); ++i) { add(p[i - 1], p[i]); add(p[i], p[i - 1]); }
+        auto acyclic = [&]() {
+            std::vector<uint8_t> seen(T, 0);
+            for (uint32_t i = 0; i < T; ++i) {
+                if (seen[i]) continue;
+                // walk the component; a component with as many edges as nodes is a cycle
+                uint32_t nodes = 0, ends = 0;
+                std::vector<int> stack{int(i)};
+                seen[i] = 1;
+                while (!stack.empty()) {
+                    int u = stack.back();
+                    stack.pop_back();
+                    ++nodes;
+                    if (deg(u) < 2) ++ends;
+                    for (int k = 0; k < 2; ++k) {
+                        int v = sn[2 * u + k];
+                        if (v >= 0 && !seen[v]) { seen[v] = 1; stack.push_back(v); }
+                    }
+                }
+                if (ends == 0 && nodes > 1) return false;
+            }
+            return true;
+        };
+        std::vector<uint8_t> onpath(T);
+        std::vector<uint8_t> bad(T, 0);
+        unsigned flips = 0;
+        bool progress = true;
+        while (progress && flips < tunnel_budget) {
+            progress = false;
+            std::fill(bad.begin(), bad.end(), uint8_t(0));   // earlier flips may open new tunnels
+            for (uint32_t s0 = 0; s0 < T && flips < tunnel_budget; ++s0) {
+                if (deg(int(s0)) >= 2 || bad[s0]) continue;
+                // depth-first search for a SIMPLE alternating path (every node at most once,
+                // so each interior degree is unchanged by the flip), bounded expansions
+                std::fill(onpath.begin(), onpath.end(), uint8_t(0));
+                std::vector<int> stk;                 // nodes of the current path, s0 first
+                std::vector<uint8_t> nexte;           // next neighbour slot to try per depth
+                stk.push_back(int(s0));
+                nexte.push_back(0);
+                onpath[s0] = 1;
+                int expansions = 0;
+                bool flipped = false;
+                while (!stk.empty() && !flipped && expansions < 4096) {
+                    const int u = stk.back(), d = int(stk.size()) - 1;
+                    const int pr = d & 1;             // even depth: next edge free; odd: strip
+                    if (nexte.back() >= 3 || d >= 24) {
+                        onpath[u] = 0;
+                        stk.pop_back();
+                        nexte.pop_back();
+                        continue;
+                    }
+                    const int v = ln[3 * u + nexte.back()++];
+                    if (v < 0 || onpath[v]) continue;
+                    if (has(u, v) != (pr == 1)) continue;
+                    ++expansions;
+                    stk.push_back(v);
+                    nexte.push_back(0);
+                    onpath[v] = 1;
+                    if (!(pr == 0 && deg(v) < 2)) continue;
+                    // free edge into a terminal: flip the tunnel (strip edges out first, then
+                    // free edges in: an interior node never holds three neighbours), keep it
+                    // if no cycle formed, else undo and keep searching
+                    std::vector<std::pair<int, int>> added, removed;
+                    for (size_t i = 1; i < stk.size(); ++i) {
+                        const int a0 = stk[i - 1], a1 = stk[i];
+                        (has(a0, a1) ? removed : added).push_back({a0, a1});
+                    }
+                    for (auto& e : removed) { del(e.first, e.second); del(e.second, e.first); }
+                    for (auto& e : added) { add(e.first, e.second); add(e.second, e.first); }
+                    if (acyclic()) { flipped = true; break; }
+                    for (auto& e : added) { del(e.first, e.second); del(e.second, e.first); }
+                    for (auto& e : removed) { add(e.first, e.second); add(e.second, e.first); }
+                }
+                ++flips;
+                if (flipped) progress = true;
+                else bad[s0] = 1;
+            }
+        }
+        // rebuild the strips from the strip-neighbour lists
+        strips.clear();
+        std::vector<uint8_t> used(T, 0);
+        for (uint32_t i = 0; i < T; ++i) {
+            if (used[i] || deg(int(i)) == 2) continue;
+            std::vector<uint16_t> path;
+            int prev = -1, u = int(i);
+            while (u >= 0) {
+                used[u] = 1;
+                path.push_back(uint16_t(u));
+                int nx = sn[2 * u] >= 0 && sn[2 * u] != prev ? sn[2 * u] : (sn[2 * u + 1] != prev ? sn[2 * u + 1] : -1);
+                if (nx >= 0 && used[nx]) nx = -1;
+                prev = u;
+                u = nx;
             }
             strips.push_back(std::move(path));
         }
