@@ -51,6 +51,9 @@ def lib():
         L.or_decode_range.restype = u32
         L.or_decode_range_u8x4.argtypes = [P, sz, u32, u32, P]
         L.or_decode_range_u8x4.restype = u32
+        L.or_decode_culled.argtypes = [P, sz, P, u32, P, P, P, P, P]
+        L.or_decode_culled.restype = u32
+        L.or_add_cull.argtypes = [P, sz, P, ctypes.POINTER(P), ctypes.POINTER(u64)]
         L.or_checksum.argtypes = [P, u64, u64]
         L.or_checksum.restype = u64
         L.or_oct_decode.argtypes = [ctypes.c_float, ctypes.c_float, P]
@@ -151,6 +154,35 @@ def decode_u8x4(blob: np.ndarray, m0=0, m1=None):
     words = np.zeros(max(info.total_tp, 1), np.uint32)
     err = lib().or_decode_range_u8x4(_p(blob), blob.nbytes, m0, m1, _p(words))
     return int(err), words[:info.total_tp]
+
+
+def decode_culled(blob: np.ndarray, view_dir, u8x4=False, want_q=True, want_f=True):
+    """Cone-culled, compacted sequential decode (FORMAT.md §7).
+    Returns (err, vis[M], counts {records, V, Tp, T}, idx, q, f) trimmed to the counts."""
+    info = blob_info(blob)
+    d = np.ascontiguousarray(np.asarray(view_dir, np.float32).reshape(3))
+    idx = np.zeros(max((1 if u8x4 else 3) * info.total_tp, 1), np.uint32)
+    q = np.zeros(max(info.n * info.total_v, 1), np.uint32) if want_q else None
+    f = np.zeros(max(info.n_out * info.total_v, 1), np.float32) if want_f else None
+    vis = np.zeros(max(info.M, 1), np.uint8)
+    cnt = np.zeros(4, np.uint64)
+    err = lib().or_decode_culled(_p(blob), blob.nbytes, _p(d), 1 if u8x4 else 0, _p(idx), _p(q), _p(f), _p(vis),
+                                 _p(cnt))
+    c = {"records": int(cnt[0]), "V": int(cnt[1]), "Tp": int(cnt[2]), "T": int(cnt[3])}
+    return (int(err), vis[:info.M].astype(bool), c, idx[:(1 if u8x4 else 3) * c["Tp"]],
+            None if q is None else q[:info.n * c["V"]], None if f is None else f[:info.n_out * c["V"]])
+
+
+def add_cull(blob: np.ndarray, entries) -> np.ndarray:
+    """Blob with the given cull table (FORMAT.md §1.5): entries (M, 4) = axis xyz, cutoff."""
+    e = np.ascontiguousarray(np.asarray(entries, np.float32).reshape(-1))
+    bp, bn = ctypes.c_void_p(), ctypes.c_uint64()
+    rc = lib().or_add_cull(_p(blob), blob.nbytes, _p(e), ctypes.byref(bp), ctypes.byref(bn))
+    if rc:
+        raise ValueError(f"add_cull failed {rc}")
+    out = np.ctypeslib.as_array(ctypes.cast(bp, ctypes.POINTER(ctypes.c_uint8)), (bn.value,)).copy()
+    lib().or_free(bp)
+    return out
 
 
 def decode_range_raw(blob, m0, m1, idx, q, f):

@@ -99,6 +99,8 @@ typedef struct {
     uint8_t bits[16], sem[16];
     uint32_t S, n_out;
     uint32_t vw;   /* FORMAT.md §1.1 flags bit 0: per-meshlet attribute widths (extension f1) */
+    uint32_t cull; /* flags bit 1: cull table present (extension f2) */
+    uint64_t off_cull;
 } or_hdr;
 
 static int parse_header(const uint8_t *b, size_t nbytes, or_hdr *h) {
@@ -112,8 +114,11 @@ static int parse_header(const uint8_t *b, size_t nbytes, or_hdr *h) {
     memcpy(h->bits, b + 96, 16);
     memcpy(h->sem, b + 112, 16);
     uint32_t flags = rd32(b + 60);
-    if (flags & ~1u) return OR_ERR_FORMAT;
+    if (flags & ~3u) return OR_ERR_FORMAT;
     h->vw = flags & 1u;
+    h->cull = (flags >> 1) & 1u;
+    h->off_cull = rd64(b + 128);
+    if (h->cull && (h->off_cull % 16u || h->off_cull + 16ull * h->M > nbytes)) return OR_ERR_FORMAT;
     if (h->codec != CODEC_GTS && h->codec != CODEC_REUSE && h->codec != CODEC_BASIC) return OR_ERR_FORMAT;
     if (h->n < 1 || h->n > 16 || h->O < 1) return OR_ERR_FORMAT;
     if (h->total_bytes != nbytes) return OR_ERR_FORMAT;
@@ -358,6 +363,83 @@ uint32_t or_decode_range_u8x4(const uint8_t *blob, size_t nbytes, uint32_t m0, u
             words[tb + t] = (tri[3 * t] & 0xFFu) | ((tri[3 * t + 1] & 0xFFu) << 8) | ((tri[3 * t + 2] & 0xFFu) << 16);
     }
     return all;
+}
+
+/* ------------------------------------------------------------------ cone culling (FORMAT.md §1.5, §7)
+ * The paper's amplification-shader cone test: record m is culled for view
+ * direction d iff fmaf(az, dz, fmaf(ay, dy, ax*dx)) > cutoff in binary32. */
+static int or_culled(const uint8_t *blob, const or_hdr *h, uint32_t m, const float *d) {
+    const uint8_t *e = blob + h->off_cull + 16ull * m;
+    float ax = rdf(e), ay = rdf(e + 4), az = rdf(e + 8), cutoff = rdf(e + 12);
+    float s = fmaf(az, d[2], fmaf(ay, d[1], ax * d[0]));
+    return s > cutoff;
+}
+
+/* Culled, compacted decode (FORMAT.md §7), sequential in record order.
+ * idx: 3*total_tp u32 (or total_tp u8x4 words when u8x4), q/f as or_decode_range (may be
+ * NULL), vis[M] (may be NULL) = 1 for visible records.  counts[4] = {visible records,
+ * sum V, sum T', sum real T}.  Returns the OR of the visible records' error bits. */
+uint32_t or_decode_culled(const uint8_t *blob, size_t nbytes, const float *d, uint32_t u8x4, uint32_t *idx,
+                          uint32_t *q, float *f, uint8_t *vis, uint64_t *counts) {
+    or_hdr h;
+    counts[0] = counts[1] = counts[2] = counts[3] = 0;
+    if (parse_header(blob, nbytes, &h) != OR_OK || !h.cull) return DERR_RECORD;
+    uint32_t all = 0;
+    uint32_t tri[3 * 256];
+    uint32_t qq[256 * 16];
+    float ff[256 * 24];
+    uint64_t VB = 0, TB = 0;
+    for (uint32_t m = 0; m < h.M; ++m) {
+        if (vis) vis[m] = 0;
+        /* never visible: empty/oversized directory span or out-of-range counts (§7) */
+        uint64_t r0 = 16ull * rd32(blob + h.off_dir + 4ull * m), r1 = 16ull * rd32(blob + h.off_dir + 4ull * (m + 1));
+        if (r1 <= r0 || r1 - r0 > h.max_record_bytes || h.off_rec + r1 > nbytes) continue;
+        const uint8_t *rec = blob + h.off_rec + r0;
+        uint32_t V = (uint32_t)rec[8] + 1u, Tp = (uint32_t)rec[9] + 1u, R = rd16(rec + 12);
+        if (V < 3u || V > h.vmax || Tp > h.tmax) continue;
+        if (or_culled(blob, &h, m, d)) continue;
+        if (vis) vis[m] = 1;
+        uint32_t meta[6] = {0};
+        uint32_t e = or_decode_meshlet(blob, nbytes, m, tri, q ? qq : NULL, f ? ff : NULL, meta);
+        all |= e;
+        if (!(e & (DERR_RECORD | DERR_COUNTS | DERR_OBJECT))) {
+            for (uint32_t t = 0; t < Tp; ++t) {
+                if (u8x4) idx[TB + t] = (tri[3 * t] & 0xFFu) | ((tri[3 * t + 1] & 0xFFu) << 8) | ((tri[3 * t + 2] & 0xFFu) << 16);
+                else for (uint32_t k = 0; k < 3; ++k) idx[3 * (TB + t) + k] = (uint32_t)VB + tri[3 * t + k];
+            }
+            if (q) memcpy(q + VB * h.n, qq, 4ull * V * h.n);
+            if (f) memcpy(f + VB * h.n_out, ff, 4ull * V * h.n_out);
+        }
+        counts[0] += 1; counts[1] += V; counts[2] += Tp; counts[3] += Tp - 4ull * (R <= Tp / 4 ? R : Tp / 4);
+        VB += V;
+        TB += Tp;
+    }
+    return all;
+}
+
+/* Insert (or replace) a cull table: entries[4*M] = {ax, ay, az, cutoff} per record.
+ * Directory offsets are relative to off_rec, so the records move as one block.
+ * Output malloc'd (free with or_free). */
+int or_add_cull(const uint8_t *blob, size_t nbytes, const float *entries, uint8_t **out, uint64_t *out_bytes) {
+    or_hdr h;
+    int st = parse_header(blob, nbytes, &h);
+    if (st) return st;
+    uint64_t base = h.cull ? h.off_cull : h.off_rec;   /* tables end where the records begin */
+    uint64_t off_cull = base, off_rec = up16(off_cull + 16ull * h.M);
+    uint64_t rec_bytes = nbytes - h.off_rec, total = off_rec + rec_bytes;
+    uint8_t *B = calloc(total, 1);
+    if (!B) return OR_ERR_NOMEM;
+    memcpy(B, blob, base);
+    for (uint32_t m = 0; m < h.M; ++m)
+        for (int k = 0; k < 4; ++k) wrf(B + off_cull + 16ull * m + 4 * k, entries[4ull * m + k]);
+    memcpy(B + off_rec, blob + h.off_rec, rec_bytes);
+    wr32(B + 60, rd32(blob + 60) | 2u);
+    wr64(B + 80, off_rec);
+    wr64(B + 88, total);
+    wr64(B + 128, off_cull);
+    *out = B;
+    *out_bytes = total;
+    return OR_OK;
 }
 
 /* ------------------------------------------------------------------ checksum (FORMAT.md §6) */
