@@ -118,7 +118,10 @@ static int parse_header(const uint8_t *b, size_t nbytes, or_hdr *h) {
     h->vw = flags & 1u;
     h->cull = (flags >> 1) & 1u;
     h->off_cull = rd64(b + 128);
-    if (h->cull && (h->off_cull % 16u || h->off_cull + 16ull * h->M > nbytes)) return OR_ERR_FORMAT;
+    /* the cull table lies between the object table and the records (FORMAT.md §1.5) */
+    if (h->cull && (h->off_cull % 16u || h->off_cull < h->off_obj + 8ull * h->n * h->O ||
+                    h->off_cull + 16ull * h->M > h->off_rec))
+        return OR_ERR_FORMAT;
     if (h->codec != CODEC_GTS && h->codec != CODEC_REUSE && h->codec != CODEC_BASIC) return OR_ERR_FORMAT;
     if (h->n < 1 || h->n > 16 || h->O < 1) return OR_ERR_FORMAT;
     if (h->total_bytes != nbytes) return OR_ERR_FORMAT;

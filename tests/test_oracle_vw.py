@@ -94,6 +94,6 @@ def test_vw_faults(orc):
     err, errs, idx, q, f = orc.decode(blob)
     assert errs[1] == orc.DERR_RECORD and errs[0] == 0
     bad = e.blob.copy()
-    bad[60] |= 2
+    bad[60] |= 4
     with pytest.raises(ValueError):
         orc.blob_info(bad)
