@@ -57,12 +57,13 @@ def log(*a):
 # ----------------------------------------------------------------------------- scenes
 
 def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: int, protos_k=(16, 91),
-               vw: bool = False):
+               vw: bool = False, cull: bool = False):
     """The rank's shard of the workload as a product-encoded blob (mc_encode path)."""
     w = WORKLOADS[workload]
     if workload == "cfg4_city":
         scene = synth.city(num_instances=instances * world, num_prototypes=protos_k[0], k=protos_k[1], seed=0)
-        protos = [mc.mc_encode(p, w["vmax"], w["tmax"], codec, variable_widths=vw) for p in scene.prototypes]
+        protos = [mc.mc_encode(p, w["vmax"], w["tmax"], codec, variable_widths=vw, cull_cones=cull)
+                  for p in scene.prototypes]
         blob = mc.mc_blob_instance_range(protos, scene.instance_proto, scene.instance_offset,
                                          rank * instances, instances)
         meta = {"instances_per_gpu": instances, "prototypes": protos_k[0],
@@ -72,7 +73,7 @@ def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: 
     mesh = {"cfg1_grid": lambda: synth.quad_grid(32, 32),
             "cfg2_torus": lambda: synth.torus(1000, 500),
             "cfg3_sphere": lambda: synth.displaced_sphere(913)}[workload]()
-    blob = mc.mc_encode(mesh, w["vmax"], w["tmax"], codec, variable_widths=vw)
+    blob = mc.mc_encode(mesh, w["vmax"], w["tmax"], codec, variable_widths=vw, cull_cones=cull)
     meta = {"restarts_per_meshlet": round(blob.encode_stats()["restarts"] / max(1, blob.layout.num_meshlets), 3)}
     if world > 1:   # strong-sharded replicas of the single mesh
         f, c = blob.shard_ranges(world)[rank]
@@ -267,17 +268,26 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     t0 = time.time()
-    blob, meta = build_blob(mc, args.workload, rank, world, args.codec, args.instances, vw=args.variable_widths)
+    blob, meta = build_blob(mc, args.workload, rank, world, args.codec, args.instances, vw=args.variable_widths,
+                            cull=args.cull)
     L = blob.layout
     log(f"[rank {rank}] scene built in {time.time() - t0:.1f}s: {L.num_meshlets} meshlets, "
         f"T={L.total_t} T'={L.total_tp} V={L.total_v}, {L.total_bytes / 1e6:.1f} MB")
     db = mc.DeviceBlob(blob, device=dev, want_vertices=True, want_quantized=False, index_format=args.index_format)
     stream = torch.cuda.current_stream(dev)
     alg_bytes = db.algorithmic_bytes()
+    view_dir = np.array([1.0, 2.0, -3.0], np.float64)
+    view_dir = (view_dir / np.linalg.norm(view_dir)).astype(np.float32)
+    if args.cull:   # FORMAT.md §7: one step = cull + scan + emit + decode of the visible records
+        step = lambda: db.decode_culled(view_dir, stream=stream)
+        launches_per_step = 4
+    else:
+        step = lambda: db.decode(stream=stream)
+        launches_per_step = 1
 
     # ---------------- device-resident timing (the headline `value`)
     for _ in range(args.warmup):
-        db.decode(stream=stream)
+        step()
     torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()
@@ -288,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
         g0.record(stream)
         for k in range(args.steps):
             ev[k][0].record(stream)
-            db.decode(stream=stream)
+            step()
             ev[k][1].record(stream)
         g1.record(stream)
         torch.cuda.synchronize(dev)
@@ -307,8 +317,18 @@ def run_ours(args, rank, world, local_rank):
     tri_all, bytes_all = float(n[0]), float(n[1])
     value = tri_all * args.steps / (max_ms * 1e-3) / 1e9
 
+    cull_info = None
+    if args.cull:
+        cc = db.read_cull_counts()
+        vis_bytes = int(alg_bytes * cc["Tp"] / max(1, L.total_tp))   # approx: bytes scale with decoded work
+        cull_info = {"view_dir": [float(x) for x in view_dir], "visible_records": cc["records"],
+                     "visible_fraction_records": cc["records"] / max(1, L.num_meshlets),
+                     "visible_triangles": cc["T"], "visible_decoded_triangles": cc["Tp"],
+                     "visible_gtri_s": cc["T"] * args.steps * world / (max_ms * 1e-3) / 1e9,
+                     "value_counts": "all scene triangles (culled ones included) per second"}
+        alg_bytes = vis_bytes
     # ---------------- verification after timing: checksum all-reduce (the only collective)
-    st = db.decode_stats(stream=stream)
+    st = db.decode_culled(view_dir, stream=stream, stats=True) if args.cull else db.decode_stats(stream=stream)
     checksum = allreduce_u64_sum([st["checksum_indices"], st["checksum_vertices"]], dist, dev)
     errs = torch.tensor([st["error_bits"]], dtype=torch.int64, device=dev)
     if dist:
@@ -316,7 +336,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- end to end through the C ABI with pinned HOST buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.cull:
         data = np.array(blob.bytes)
         h_blob = torch.from_numpy(data).pin_memory()
         idx_words = (1 if args.index_format == "u8x4" else 3) * L.total_tp
@@ -377,7 +397,8 @@ def run_ours(args, rank, world, local_rank):
         "hbm_gbs_aggregate": bytes_all * args.steps / (max_ms * 1e-3) / 1e9,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * launches_per_step,
+        "cull": cull_info,
         "clocks": clk.summary(),
         "checksum": {"indices": checksum[0], "vertices": checksum[1], "error_bits": int(errs.item())},
     }
@@ -394,6 +415,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=list(WORKLOADS), default="cfg4_city")
     ap.add_argument("--codec", type=int, default=2, choices=[1, 2, 3], help="1 GTS, 2 GTS-Reuse, 3 Basic")
+    ap.add_argument("--cull", action="store_true",
+                    help="cone-culled compacted decode (FORMAT.md §7, extension f2) for a fixed view direction")
     ap.add_argument("--variable-widths", action="store_true",
                     help="per-meshlet attribute code widths (FORMAT.md VW, extension f1)")
     ap.add_argument("--index-format", default="u32", choices=["u32", "u8x4"],

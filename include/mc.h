@@ -79,9 +79,12 @@ typedef struct {
 } mc_mesh;
 
 enum {
-    MC_ENCODE_VARIABLE_WIDTHS = 1   /* per-meshlet attribute code widths w_c = bit length of the
+    MC_ENCODE_VARIABLE_WIDTHS = 1,  /* per-meshlet attribute code widths w_c = bit length of the
                                        meshlet's largest code on the unchanged global grid
                                        (FORMAT.md §1.4 VW, motivated by P:715–716) */
+    MC_ENCODE_CULL_CONES = 2        /* per-meshlet normal cones (FORMAT.md §1.5 cull table) from the
+                                       decoded positions, for mc_decode_culled;
+                                       MC_ERR_ARG if the mesh has fewer than 3 position channels */
 };
 
 typedef struct {
@@ -102,7 +105,9 @@ typedef struct {
     uint32_t base_meshlet, base_vtx, base_tri, max_record_bytes;
     uint64_t off_dir, off_obj, off_rec, total_bytes;
     uint8_t bits[16], semantic[16];   /* global grid widths b_c and semantics          */
-    uint32_t flags;                   /* BlobHeader flags (bit 0 VW: per-record widths) */
+    uint32_t flags;                   /* BlobHeader flags (bit 0 VW: per-record widths,
+                                         bit 1 CULL: cull table at off_cull)            */
+    uint64_t off_cull;                /* FORMAT.md §1.5, 0 without CULL                 */
 } mc_layout;
 
 /* Encode a mesh (P:279–305 meshlets; P:312–467 strips; P:486–492 quantisation).
@@ -197,6 +202,22 @@ mc_status mc_decode_meshlets(const mc_decode_args *args, void *stream);
 
 /* Same decode, additionally accumulating mc_stats into *d_stats (device). */
 mc_status mc_decode_stats(const mc_decode_args *args, mc_stats *d_stats, void *stream);
+
+/* Cone-culled, compacted decode (FORMAT.md §1.5, §7; the paper's amplification-shader
+ * cone culling).  For the unit view direction view_dir (host,
+ * float[3], from the camera into the scene; a directional / orthographic view), every
+ * record whose cone test fmaf(az,dz,fmaf(ay,dy,ax*dx)) > cutoff (binary32) holds is
+ * skipped; the visible records are decoded in record order into compacted outputs
+ * (index/vertex positions and u32 index values relative to 0).  args must cover the
+ * whole blob (first = 0, count = num_meshlets); output buffers are sized as for
+ * mc_decode_meshlets (the visible part is a prefix of them).  d_counts (device,
+ * uint32_t[4]) receives {visible records, Σ V, Σ T', Σ T (real)}; d_stats (device or
+ * NULL) accumulates mc_stats over the visible records.  d_scratch: device, 16-B aligned,
+ * >= mc_decode_culled_scratch_bytes(layout).  Asynchronous: four kernels on `stream`.
+ * Errors: MC_ERR_FORMAT (blob without cull table), MC_ERR_ARG, MC_ERR_LIMITS, MC_ERR_CUDA. */
+size_t mc_decode_culled_scratch_bytes(const mc_layout *layout);
+mc_status mc_decode_culled(const mc_decode_args *args, const float *view_dir, void *d_scratch, size_t scratch_bytes,
+                           uint32_t *d_counts, mc_stats *d_stats, void *stream);
 
 /* Initialise a device mc_stats: zeros, first_bad_meshlet = UINT32_MAX. */
 mc_status mc_stats_reset(mc_stats *d_stats, void *stream);

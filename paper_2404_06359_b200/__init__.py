@@ -21,7 +21,7 @@ LIB_PATH = _build.LIB
 
 MC_CODEC_GTS, MC_CODEC_GTS_REUSE, MC_CODEC_BASIC = 1, 2, 3
 MC_DECODE_BLOB_LOCAL_INDICES, MC_DECODE_INDEX_LOCAL_U8X4 = 1, 2
-MC_ENCODE_VARIABLE_WIDTHS = 1
+MC_ENCODE_VARIABLE_WIDTHS, MC_ENCODE_CULL_CONES = 1, 2
 ABI_VERSION = 2
 MC_DERR_RECORD, MC_DERR_COUNTS, MC_DERR_INDEX, MC_DERR_REUSE, MC_DERR_OBJECT = 1, 2, 4, 8, 16
 
@@ -36,7 +36,7 @@ class mc_layout(ctypes.Structure):
                  "total_v", "total_tp", "total_t", "base_meshlet", "base_vtx", "base_tri", "max_record_bytes")] + \
                [("off_dir", ctypes.c_uint64), ("off_obj", ctypes.c_uint64), ("off_rec", ctypes.c_uint64),
                 ("total_bytes", ctypes.c_uint64), ("bits", ctypes.c_uint8 * 16), ("semantic", ctypes.c_uint8 * 16),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("off_cull", ctypes.c_uint64)]
 
 
 class mc_mesh(ctypes.Structure):
@@ -76,7 +76,7 @@ STATS_BYTES = ctypes.sizeof(mc_stats)
 EXPORTS = ["mc_encode", "mc_blob_instance", "mc_blob_instance_range", "mc_blob_from_bytes", "mc_blob_bytes", "mc_blob_source_map",
            "mc_blob_encode_stats", "mc_blob_free", "mc_parse_header", "mc_blob_shard_ranges", "mc_blob_extract",
            "mc_decode_meshlets", "mc_decode_stats", "mc_stats_reset", "mc_decode_host", "mc_status_str",
-           "mc_abi_version"]
+           "mc_abi_version", "mc_decode_culled", "mc_decode_culled_scratch_bytes"]
 
 _lib = None
 
@@ -112,6 +112,9 @@ def lib() -> ctypes.CDLL:
         L.mc_stats_reset.argtypes = [P, P]
         L.mc_decode_host.argtypes = [ctypes.POINTER(mc_host_decode_args), P]
         L.mc_status_str.argtypes = [ctypes.c_int]
+        L.mc_decode_culled.argtypes = [ctypes.POINTER(mc_decode_args), P, P, sz, P, P, P]
+        L.mc_decode_culled_scratch_bytes.argtypes = [ctypes.POINTER(mc_layout)]
+        L.mc_decode_culled_scratch_bytes.restype = sz
         _lib = L
     return _lib
 
@@ -193,7 +196,7 @@ def parse_header(data: np.ndarray) -> mc_layout:
 
 
 def mc_encode(mesh, max_vertices: int = 64, max_triangles: int = 126, codec: int = MC_CODEC_GTS_REUSE,
-              num_threads: int = 0, variable_widths: bool = False) -> Blob:
+              num_threads: int = 0, variable_widths: bool = False, cull_cones: bool = False) -> Blob:
     """Encode a mesh (any object with indices/attributes/bits/semantic[/object_of_triangle]);
     ``variable_widths``: per-meshlet attribute code widths (MC_ENCODE_VARIABLE_WIDTHS)."""
     idx = np.ascontiguousarray(mesh.indices, dtype=np.uint32)
@@ -205,7 +208,8 @@ def mc_encode(mesh, max_vertices: int = 64, max_triangles: int = 126, codec: int
     m = mc_mesh(attr.shape[0], idx.reshape(-1, 3).shape[0], _p(idx), _p(attr), attr.shape[1], _p(bits), _p(sem),
                 _p(obj))
     prm = mc_encode_params(max_vertices, max_triangles, codec, num_threads,
-                           MC_ENCODE_VARIABLE_WIDTHS if variable_widths else 0)
+                           (MC_ENCODE_VARIABLE_WIDTHS if variable_widths else 0) |
+                           (MC_ENCODE_CULL_CONES if cull_cones else 0))
     h = ctypes.c_void_p()
     _check(lib().mc_encode(ctypes.byref(m), ctypes.byref(prm), ctypes.byref(h)), "mc_encode")
     return Blob(h)
@@ -339,6 +343,32 @@ class DeviceBlob:
         mc_decode_stats(self.layout, self.d_blob, self.indices, self.stats, self.vertices, self.quantized, first,
                         count, flags | self.index_flags, stream)
         return read_stats(self.stats)
+
+    def decode_culled(self, view_dir, stream=None, flags=0, stats=False):
+        """Enqueue the cone-culled compacted decode (FORMAT.md §7) for a unit view direction;
+        counts land in ``self.cull_counts`` (device int32[4]: records, V, T', T)."""
+        import torch
+        L = self.layout
+        if getattr(self, "cull_scratch", None) is None:
+            nb = lib().mc_decode_culled_scratch_bytes(ctypes.byref(L))
+            self.cull_scratch = torch.empty((nb + 15) // 16 * 16, dtype=torch.uint8, device=self.d_blob.device)
+            self.cull_counts = torch.zeros(4, dtype=torch.int32, device=self.d_blob.device)
+        _check_sizes(L, self.d_blob, self.indices, self.vertices, self.quantized, flags | self.index_flags)
+        a = mc_decode_args(ctypes.pointer(L), self.d_blob.data_ptr(), 0, L.num_meshlets, self.indices.data_ptr(),
+                           None if self.vertices is None else self.vertices.data_ptr(),
+                           None if self.quantized is None else self.quantized.data_ptr(), flags | self.index_flags)
+        d = (ctypes.c_float * 3)(*[float(x) for x in view_dir])
+        if stats:
+            mc_stats_reset(self.stats, stream)
+        _check(lib().mc_decode_culled(ctypes.byref(a), ctypes.cast(d, ctypes.c_void_p), self.cull_scratch.data_ptr(),
+                                      self.cull_scratch.numel(), self.cull_counts.data_ptr(),
+                                      self.stats.data_ptr() if stats else None, _stream_handle(stream)),
+               "mc_decode_culled")
+        return read_stats(self.stats) if stats else None
+
+    def read_cull_counts(self) -> dict:
+        c = self.cull_counts.cpu().numpy().view(np.uint32)
+        return {"records": int(c[0]), "V": int(c[1]), "Tp": int(c[2]), "T": int(c[3])}
 
     def algorithmic_bytes(self) -> int:
         """Compressed bytes read (directory + records + object table) + decompressed bytes written."""

@@ -61,7 +61,7 @@ namespace {
 constexpr int kWarpsPerCta = 8;
 constexpr int kThreads = kWarpsPerCta * 32;
 constexpr uint32_t kFull = 0xFFFFFFFFu;
-constexpr uint32_t kMiscWords = 112;   // 2 mbarriers, 2 sizes, 32 consts, N[272 B]
+constexpr uint32_t kMiscWords = 120;   // 2 mbarriers, 2 sizes, 32 consts, N[288 B], list bases[4]
 
 struct Params {
     const uint8_t* rec;        // records section
@@ -75,6 +75,8 @@ struct Params {
     uint32_t u8x4;             // MC_DECODE_INDEX_LOCAL_U8X4: one local u8x4 word per triangle
     uint32_t hdr_words;        // record header words (16 + 4n [+ n with VW] rounded to 16) / 4
     uint32_t vw;               // FORMAT.md VW: per-record attribute widths w_c after L_c
+    const uint4* list;         // culled decode (FORMAT.md §7): visible records {m, VB, TB, 0}, or null
+    const uint32_t* list_count;// device count of list entries
     uint32_t buf_words;        // per-buffer words (max_rec/4 + 4)
     uint32_t vtx_stage_words;  // vmax*n_out + 8 for the generic layout, else 0
     uint32_t grp_words;        // smem words per group: 2 buffers + vertex stage + misc, padded
@@ -225,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
     uint32_t* sizes = misc + 4;                                       // staged bytes per buffer
     float* consts = reinterpret_cast<float*>(misc + 8);               // Δ[16], g[16] (generic path)
     uint8_t* Nbuf = reinterpret_cast<uint8_t*>(misc + 40);            // N[0..T'+1], 272 B
+    uint32_t* lbase = misc + 112;                                     // list mode: VB[2], TB[2] per buffer
 
     const uint32_t ngroups = gridDim.x * wpc * NG;
     const uint32_t gg = blockIdx.x * wpc * NG + gslot;
@@ -234,10 +237,13 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
     uint32_t m = P.first + min(gg * per, P.end - P.first);
     const uint32_t mstop = min(P.end, m + per), mstep = 1;
 #else
-    // grid stride: neighbouring groups decode neighbouring records
-    uint32_t m = P.first + gg;
-    const uint32_t mstop = P.end, mstep = ngroups;
+    // grid stride: neighbouring groups decode neighbouring records (list mode: neighbouring
+    // entries of the visible-record list of a culled decode, FORMAT.md §7)
+    uint32_t m = P.list ? gg : P.first + gg;
+    const uint32_t mstop = P.list ? min(*P.list_count, P.end) : P.end, mstep = ngroups;
 #endif
+    // record id of sequence position i (identity, or the culled decode's visible list)
+    auto rid = [&](uint32_t i) -> uint32_t { return P.list ? __ldg(&P.list[i].x) : i; };
 
     if (gl == 0) {
         mbar_init(&bars[0], 1);
@@ -248,7 +254,12 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
 
     // a2: lane 0 of the group stages record `mm` with one TMA bulk copy into buffer `b`
     // (or a plain arrive for a record that cannot be staged: size 0 -> RECORD error)
-    auto issue = [&](uint32_t d0, uint32_t d1, int b) {
+    auto issue = [&](uint32_t d0, uint32_t d1, int b, uint32_t pos) {
+        if (P.list) {
+            const uint4 e = __ldg(&P.list[pos]);
+            lbase[b] = e.y;
+            lbase[2 + b] = e.z;
+        }
         const uint64_t off = 16ull * d0;
         const uint32_t bytes = (d1 > d0) ? 16u * (d1 - d0) : 0u;
         const bool ok = bytes != 0 && bytes <= P.max_rec && off + bytes <= P.rec_section_bytes;
@@ -264,8 +275,13 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
 
     uint32_t nd0 = 0, nd1 = 0;   // directory entries of the record after next (prefetched)
     if (m < mstop && gl == 0) {
-        issue(__ldg(P.dir + m), __ldg(P.dir + m + 1), 0);
-        if (m + mstep < mstop) { nd0 = __ldg(P.dir + m + mstep); nd1 = __ldg(P.dir + m + mstep + 1); }
+        const uint32_t r0 = rid(m);
+        issue(__ldg(P.dir + r0), __ldg(P.dir + r0 + 1), 0, m);
+        if (m + mstep < mstop) {
+            const uint32_t r1 = rid(m + mstep);
+            nd0 = __ldg(P.dir + r1);
+            nd1 = __ldg(P.dir + r1 + 1);
+        }
     }
 
     WarpStats ws;
@@ -274,9 +290,13 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
         const int b = k & 1;
         const uint32_t mnext = m + mstep;
         if (gl == 0 && mnext < mstop) {
-            issue(nd0, nd1, b ^ 1);
+            issue(nd0, nd1, b ^ 1, mnext);
             const uint32_t m2 = mnext + mstep;
-            if (m2 < mstop) { nd0 = __ldg(P.dir + m2); nd1 = __ldg(P.dir + m2 + 1); }
+            if (m2 < mstop) {
+                const uint32_t r2 = rid(m2);
+                nd0 = __ldg(P.dir + r2);
+                nd1 = __ldg(P.dir + r2 + 1);
+            }
         }
         mbar_wait(&bars[b], (k >> 1) & 1);
         __syncwarp(gm);
@@ -284,7 +304,8 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
         const uint32_t staged = sizes[b];
 
         // ---------------- a1: header (FORMAT.md §1.4) + structural validation (§5)
-        const uint32_t vtx_base = R[0], tri_base = R[1], w2 = R[2];
+        // list mode: compacted output bases of this visible record (FORMAT.md §7)
+        const uint32_t vtx_base = P.list ? lbase[b] : R[0], tri_base = P.list ? lbase[2 + b] : R[1], w2 = R[2];
         const uint32_t V = (w2 & 0xFFu) + 1u, Tp = ((w2 >> 8) & 0xFFu) + 1u, object = w2 >> 16;
         const uint32_t W = CODEC == MC_CODEC_BASIC ? 0u : (Tp + 31u) >> 5;   // Basic: no flag words
         const uint32_t nb = (CODEC == MC_CODEC_GTS) ? (Tp - 1u)
@@ -346,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
             if (err) {
                 if (STATS && gl == 0) {
                     atomicOr(&P.stats->error_bits, err);
-                    atomicMin(&P.stats->first_bad_meshlet, m);
+                    atomicMin(&P.stats->first_bad_meshlet, rid(m));
                     atomicAdd(&P.stats->num_bad, 1u);
                 }
                 __syncwarp(gm);
@@ -396,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
         if (err) {
             if (STATS && gl == 0) {
                 atomicOr(&P.stats->error_bits, err);
-                atomicMin(&P.stats->first_bad_meshlet, m);
+                atomicMin(&P.stats->first_bad_meshlet, rid(m));
                 atomicAdd(&P.stats->num_bad, 1u);
             }
             __syncwarp(gm);
@@ -457,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
                 ws.verts += V;
                 if (e2) {
                     atomicOr(&P.stats->error_bits, e2);
-                    atomicMin(&P.stats->first_bad_meshlet, m);
+                    atomicMin(&P.stats->first_bad_meshlet, rid(m));
                     atomicAdd(&P.stats->num_bad, 1u);
                 }
             }
@@ -643,6 +664,112 @@ __global__ void stats_reset_kernel(mc_stats* s) {
     }
 }
 
+// ------------------------------------------------------------------ cone culling (FORMAT.md §1.5, §7)
+// The paper's amplification-shader pass: per record, the binary32 cone test
+// fmaf(az,dz, fmaf(ay,dy, ax*dx)) > cutoff, then a three-kernel reduce / scan / emit that
+// lists the visible records in record order with their compacted output bases.  The
+// decode kernel then walks that list (Params::list).
+constexpr int kCullThreads = 256, kCullPerThread = 8, kCullTile = kCullThreads * kCullPerThread;
+
+struct CullParams {
+    const uint8_t* rec;
+    const uint32_t* dir;
+    const float4* cones;
+    uint64_t rec_section_bytes;
+    uint32_t M, vmax, tmax, max_rec;
+    float dx, dy, dz;
+    uint4* tile_sum;      // [tiles] {records, V, T', T}
+    uint4* tile_off;      // [tiles] exclusive prefix of tile_sum
+    uint4* list;          // [M] {m, VB, TB, 0}
+    uint32_t* counts;     // [4] totals {records, V, T', T}
+    uint32_t tiles;
+};
+
+// visibility of record m and its counts (0 when not visible)
+__device__ __forceinline__ uint4 cull_one(const CullParams& C, uint32_t m) {
+    if (m >= C.M) return make_uint4(0, 0, 0, 0);
+    const uint32_t d0 = __ldg(C.dir + m), d1 = __ldg(C.dir + m + 1);
+    const uint64_t bytes = 16ull * (d1 - d0);
+    if (d1 <= d0 || bytes > C.max_rec || 16ull * d0 + bytes > C.rec_section_bytes) return make_uint4(0, 0, 0, 0);
+    const uint4 h = __ldg(reinterpret_cast<const uint4*>(C.rec + 16ull * d0));
+    const uint32_t V = (h.z & 0xFFu) + 1u, Tp = ((h.z >> 8) & 0xFFu) + 1u, R = h.w & 0xFFFFu;
+    if (V < 3u || V > C.vmax || Tp > C.tmax) return make_uint4(0, 0, 0, 0);
+    const float4 c = __ldg(C.cones + m);
+    const float sdot = __fmaf_rn(c.z, C.dz, __fmaf_rn(c.y, C.dy, __fmul_rn(c.x, C.dx)));
+    if (sdot > c.w) return make_uint4(0, 0, 0, 0);                     // culled: all back-facing
+    return make_uint4(1u, V, Tp, Tp - 4u * min(R, Tp / 4u));
+}
+
+__device__ __forceinline__ uint4 add4(uint4 a, uint4 b) { return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ uint4 shfl_up4(uint4 v, int d) {
+    return make_uint4(__shfl_up_sync(kFull, v.x, d), __shfl_up_sync(kFull, v.y, d), __shfl_up_sync(kFull, v.z, d),
+                      __shfl_up_sync(kFull, v.w, d));
+}
+// block-wide inclusive scan of one uint4 per thread (kCullThreads threads)
+__device__ __forceinline__ uint4 block_scan4(uint4 v, uint4* sh /* [kCullThreads/32] */) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint4 o = shfl_up4(v, d);
+        if (lane >= d) v = add4(v, o);
+    }
+    if (lane == 31) sh[wid] = v;
+    __syncthreads();
+    uint4 pre = make_uint4(0, 0, 0, 0);
+    for (int w = 0; w < wid; ++w) pre = add4(pre, sh[w]);
+    __syncthreads();
+    return add4(v, pre);
+}
+
+__global__ void __launch_bounds__(kCullThreads) cull_reduce_kernel(const CullParams C) {
+    __shared__ uint4 sh[kCullThreads / 32];
+    const uint32_t base = blockIdx.x * kCullTile + threadIdx.x * kCullPerThread;
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < kCullPerThread; ++i) acc = add4(acc, cull_one(C, base + i));
+    const uint4 inc = block_scan4(acc, sh);
+    if (threadIdx.x == kCullThreads - 1) C.tile_sum[blockIdx.x] = inc;
+}
+
+__global__ void __launch_bounds__(kCullThreads) cull_scan_tiles_kernel(const CullParams C) {
+    __shared__ uint4 sh[kCullThreads / 32];
+    __shared__ uint4 chunk_total;
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    for (uint32_t t0 = 0; t0 < C.tiles; t0 += kCullThreads) {
+        const uint32_t t = t0 + threadIdx.x;
+        const uint4 v = t < C.tiles ? C.tile_sum[t] : make_uint4(0, 0, 0, 0);
+        const uint4 inc = block_scan4(v, sh);
+        if (t < C.tiles) C.tile_off[t] = add4(carry, make_uint4(inc.x - v.x, inc.y - v.y, inc.z - v.z, inc.w - v.w));
+        if (threadIdx.x == kCullThreads - 1) chunk_total = inc;
+        __syncthreads();
+        carry = add4(carry, chunk_total);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        C.counts[0] = carry.x;
+        C.counts[1] = carry.y;
+        C.counts[2] = carry.z;
+        C.counts[3] = carry.w;
+    }
+}
+
+__global__ void __launch_bounds__(kCullThreads) cull_emit_kernel(const CullParams C) {
+    __shared__ uint4 sh[kCullThreads / 32];
+    const uint32_t base = blockIdx.x * kCullTile + threadIdx.x * kCullPerThread;
+    uint4 v[kCullPerThread];
+    uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int i = 0; i < kCullPerThread; ++i) {
+        v[i] = cull_one(C, base + i);
+        acc = add4(acc, v[i]);
+    }
+    const uint4 inc = block_scan4(acc, sh);
+    uint4 run = add4(C.tile_off[blockIdx.x], make_uint4(inc.x - acc.x, inc.y - acc.y, inc.z - acc.z, inc.w - acc.w));
+#pragma unroll
+    for (int i = 0; i < kCullPerThread; ++i) {
+        if (v[i].x) C.list[run.x] = make_uint4(base + i, run.y, run.z, 0u);
+        run = add4(run, v[i]);
+    }
+}
+
 // ------------------------------------------------------------------ host launch
 mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t& smem) {
     if (!a || !a->layout) return MC_ERR_ARG;
@@ -677,6 +804,8 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     P.index_sub = (a->flags & MC_DECODE_BLOB_LOCAL_INDICES) ? L.base_vtx : 0u;
     P.u8x4 = (a->flags & MC_DECODE_INDEX_LOCAL_U8X4) ? 1u : 0u;
     P.vw = L.flags & 1u;
+    P.list = nullptr;
+    P.list_count = nullptr;
     P.hdr_words = ((16u + 4u * L.n + (P.vw ? L.n : 0u) + 15u) & ~15u) / 4u;
     P.buf_words = L.max_record_bytes / 4u + 4u;
     P.vtx_stage_words = 0;
@@ -789,11 +918,19 @@ mc_status dispatch_codec(uint32_t codec, bool stats, int lay, int am, const Para
                  : dispatch_layout<MC_CODEC_GTS_REUSE, false>(lay, am, P, smem, s);
 }
 
-mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s) {
+mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s, const uint4* list = nullptr,
+                 const uint32_t* list_count = nullptr) {
     Params P;
     size_t smem = 0;
     mc_status rc = build_params(a, st, P, smem);
     if (rc != MC_OK) return rc;
+    P.list = list;
+    P.list_count = list_count;
+    if (list) {   // culled decode: compacted outputs start at 0 (FORMAT.md §7)
+        P.base_vtx = 0;
+        P.base_tri = 0;
+        P.index_sub = 0;
+    }
     if (a->count == 0) return MC_OK;
     // compile-time layouts for the BASELINE configs, generic kernel otherwise
     const mc_layout& L = *a->layout;
@@ -830,6 +967,50 @@ mc_status mc_decode_meshlets(const mc_decode_args* args, void* stream) {
 mc_status mc_decode_stats(const mc_decode_args* args, mc_stats* d_stats, void* stream) {
     if (!d_stats) return MC_ERR_ARG;
     return launch(args, d_stats, static_cast<cudaStream_t>(stream));
+}
+
+size_t mc_decode_culled_scratch_bytes(const mc_layout* L) {
+    if (!L) return 0;
+    const uint64_t tiles = (uint64_t(L->num_meshlets) + kCullTile - 1) / kCullTile;
+    return size_t(16ull * L->num_meshlets + 32ull * tiles + 16ull);
+}
+
+mc_status mc_decode_culled(const mc_decode_args* a, const float* view_dir, void* d_scratch, size_t scratch_bytes,
+                           uint32_t* d_counts, mc_stats* d_stats, void* stream) {
+    if (!a || !a->layout || !view_dir || !d_counts) return MC_ERR_ARG;
+    const mc_layout& L = *a->layout;
+    if (!(L.flags & 2u) || L.off_cull == 0) return MC_ERR_FORMAT;            // no cull table
+    if (a->first != 0 || a->count != L.num_meshlets) return MC_ERR_ARG;      // whole blob only
+    if (reinterpret_cast<uintptr_t>(d_counts) & 3u) return MC_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t M = L.num_meshlets;
+    if (M == 0) return cudaMemsetAsync(d_counts, 0, 16, s) == cudaSuccess ? MC_OK : MC_ERR_CUDA;
+    if (!a->d_blob || (reinterpret_cast<uintptr_t>(a->d_blob) & 15u)) return MC_ERR_ARG;
+    if (!d_scratch || (reinterpret_cast<uintptr_t>(d_scratch) & 15u) || scratch_bytes < mc_decode_culled_scratch_bytes(&L))
+        return MC_ERR_ARG;
+    const uint8_t* blob = static_cast<const uint8_t*>(a->d_blob);
+    CullParams C;
+    C.rec = blob + L.off_rec;
+    C.dir = reinterpret_cast<const uint32_t*>(blob + L.off_dir);
+    C.cones = reinterpret_cast<const float4*>(blob + L.off_cull);
+    C.rec_section_bytes = L.total_bytes - L.off_rec;
+    C.M = M;
+    C.vmax = L.v_max;
+    C.tmax = L.t_max;
+    C.max_rec = L.max_record_bytes;
+    C.dx = view_dir[0];
+    C.dy = view_dir[1];
+    C.dz = view_dir[2];
+    C.tiles = (M + kCullTile - 1) / kCullTile;
+    C.list = static_cast<uint4*>(d_scratch);
+    C.tile_sum = C.list + M;
+    C.tile_off = C.tile_sum + C.tiles;
+    C.counts = d_counts;
+    cull_reduce_kernel<<<C.tiles, kCullThreads, 0, s>>>(C);
+    cull_scan_tiles_kernel<<<1, kCullThreads, 0, s>>>(C);
+    cull_emit_kernel<<<C.tiles, kCullThreads, 0, s>>>(C);
+    if (cudaGetLastError() != cudaSuccess) return MC_ERR_CUDA;
+    return launch(a, d_stats, s, C.list, d_counts);
 }
 
 mc_status mc_stats_reset(mc_stats* d_stats, void* stream) {

@@ -11,6 +11,8 @@
 #include "../../include/mc.h"
 
 #include <algorithm>
+#include <array>
+#include <unordered_map>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -105,6 +107,7 @@ struct Encoder {
     std::vector<int32_t> vlocal;         // scratch: vertex -> local index during emission
 
     bool vw = false;                     // MC_ENCODE_VARIABLE_WIDTHS
+    bool cull = false;                   // MC_ENCODE_CULL_CONES
     Encoder(const mc_mesh& m, uint32_t vm, uint32_t tm, uint32_t cd, unsigned th, bool varw = false)
         : mesh(m), vmax(vm), tmax(tm), codec(cd), threads(th), n(m.num_channels), S(0), vw(varw) {
         for (uint32_t c = 0; c < n; ++c) S += m.bits[c];
@@ -601,7 +604,8 @@ namespace {
 void write_header(uint8_t* B, uint32_t codec, uint32_t n, uint32_t M, uint32_t O, uint32_t vmax,
                   uint32_t tmax, uint64_t tv, uint64_t ttp, uint64_t tt, uint32_t base_m, uint32_t base_v,
                   uint32_t base_t, uint32_t maxrec, uint64_t off_dir, uint64_t off_obj, uint64_t off_rec,
-                  uint64_t total, const uint8_t* bits, const uint8_t* sem, uint32_t flags = 0) {
+                  uint64_t total, const uint8_t* bits, const uint8_t* sem, uint32_t flags = 0,
+                  uint64_t off_cull = 0) {
     std::memcpy(B, "MCZ1", 4);
     put32(B + 4, 1); put32(B + 8, codec); put32(B + 12, n); put32(B + 16, M); put32(B + 20, O);
     put32(B + 24, vmax); put32(B + 28, tmax); put32(B + 32, uint32_t(tv)); put32(B + 36, uint32_t(ttp));
@@ -610,6 +614,46 @@ void write_header(uint8_t* B, uint32_t codec, uint32_t n, uint32_t M, uint32_t O
     put64(B + 64, off_dir); put64(B + 72, off_obj); put64(B + 80, off_rec); put64(B + 88, total);
     std::memset(B + 96, 0, 64);
     for (uint32_t c = 0; c < n; ++c) { B[96 + c] = bits[c]; B[112 + c] = sem[c]; }
+    put64(B + 128, off_cull);
+}
+
+// Normal cone of one meshlet from its DECODED positions (FORMAT.md §1.5/§7):
+// axis = normalised sum of the real triangles' unit normals, θ = largest angle between the
+// stored (binary32) axis and any of them, plus a margin for binary32 rounding of the test
+// and of translated grid origins (instancing); cutoff = sin θ rounded up, or 2 (never).
+void cull_cone(const std::vector<std::array<double, 3>>& P, const std::vector<std::array<uint32_t, 3>>& tris,
+               float out[4]) {
+    constexpr double kMargin = 0.01;   // radians
+    std::vector<std::array<double, 3>> nrm;
+    double sx = 0, sy = 0, sz = 0;
+    for (auto& t : tris) {
+        const auto &a = P[t[0]], &b = P[t[1]], &c = P[t[2]];
+        const double ux = b[0] - a[0], uy = b[1] - a[1], uz = b[2] - a[2];
+        const double vx = c[0] - a[0], vy = c[1] - a[1], vz = c[2] - a[2];
+        double nx = uy * vz - uz * vy, ny = uz * vx - ux * vz, nz = ux * vy - uy * vx;
+        const double l = std::sqrt(nx * nx + ny * ny + nz * nz);
+        if (!(l > 0)) continue;                      // zero area after quantisation: no facing
+        nx /= l; ny /= l; nz /= l;
+        nrm.push_back({nx, ny, nz});
+        sx += nx; sy += ny; sz += nz;
+    }
+    const double sl = std::sqrt(sx * sx + sy * sy + sz * sz);
+    out[0] = 0.0f; out[1] = 0.0f; out[2] = 1.0f; out[3] = 2.0f;   // never cull
+    if (nrm.empty() || sl < 1e-6 * double(nrm.size())) return;
+    const float ax = float(sx / sl), ay = float(sy / sl), az = float(sz / sl);
+    const double al = std::sqrt(double(ax) * ax + double(ay) * ay + double(az) * az);
+    double theta = 0;
+    for (auto& n : nrm) {
+        double cs = (n[0] * ax + n[1] * ay + n[2] * az) / al;
+        theta = std::max(theta, std::acos(std::max(-1.0, std::min(1.0, cs))));
+    }
+    theta += kMargin;
+    out[0] = ax; out[1] = ay; out[2] = az;
+    if (theta >= 1.5707963267948966) return;
+    const double sc = std::sin(theta);
+    float c = float(sc);
+    if (double(c) < sc) c = std::nextafter(c, 2.0f);
+    out[3] = c;
 }
 
 // Quantise and serialise (FORMAT.md §1, §3).
@@ -647,7 +691,11 @@ mc_status serialise(Encoder& E, mc_blob& out) {
         }
     std::vector<uint32_t> Lq(M * n);
     std::vector<uint8_t> wq(M * n);    // per-meshlet code widths (VW) or the global b_c
-    const bool vw = E.vw;
+    const bool vw = E.vw, cull = E.cull;
+    uint32_t pos_ch[3] = {0, 0, 0}, npos = 0;
+    for (uint32_t c = 0; c < n && npos < 3; ++c)
+        if (mesh.semantic[c] == MC_SEM_POSITION) pos_ch[npos++] = c;
+    if (cull && npos < 3) return MC_ERR_ARG;
     auto qof = [](float x, float g, float d) { return std::floor((double(x) - double(g)) / double(d) + 0.5); };
     for (uint32_t o = 0; o < O; ++o)
         for (uint32_t c = 0; c < n; ++c) {
@@ -701,11 +749,13 @@ mc_status serialise(Encoder& E, mc_blob& out) {
     }
     if (tv > 0xFFFFFFFFull || 3 * ttp > 0xFFFFFFFFull || roff[M] / 16 > 0xFFFFFFFFull) return MC_ERR_RANGE;
     const uint64_t off_dir = kHeaderBytes, off_obj = round16(off_dir + 4ull * (M + 1));
-    const uint64_t off_rec = round16(off_obj + 8ull * n * O), total = off_rec + roff[M];
+    const uint64_t off_cull = cull ? round16(off_obj + 8ull * n * O) : 0;
+    const uint64_t off_rec = cull ? round16(off_cull + 16ull * M) : round16(off_obj + 8ull * n * O);
+    const uint64_t total = off_rec + roff[M];
     if (!out.allocate(total)) return MC_ERR_NOMEM;
     uint8_t* B = out.bytes;
     write_header(B, codec, n, uint32_t(M), O, E.vmax, E.tmax, tv, ttp, tt, 0, 0, 0, uint32_t(maxrec), off_dir,
-                 off_obj, off_rec, total, mesh.bits, mesh.semantic, vw ? 1u : 0u);
+                 off_obj, off_rec, total, mesh.bits, mesh.semantic, (vw ? 1u : 0u) | (cull ? 2u : 0u), off_cull);
     for (size_t m = 0; m <= M; ++m) put32(B + off_dir + 4 * m, uint32_t(roff[m] / 16));
     for (uint32_t o = 0; o < O; ++o)
         for (uint32_t c = 0; c < n; ++c) {
@@ -757,6 +807,27 @@ mc_status serialise(Encoder& E, mc_blob& out) {
             out.src_vertex[vb[m] + v] = me.local_to_src[v];
         }
         for (uint32_t t = 0; t < me.Tp; ++t) out.src_tri[tb[m] + t] = me.src_tri[t];
+        if (cull) {
+            // decoded positions exactly as a decoder computes them (FORMAT.md §3)
+            std::vector<std::array<double, 3>> Pd(me.V);
+            std::unordered_map<uint32_t, uint32_t> loc;
+            for (uint32_t v = 0; v < me.V; ++v) {
+                loc[me.local_to_src[v]] = v;
+                const float* A = mesh.attributes + uint64_t(me.local_to_src[v]) * n;
+                for (int k = 0; k < 3; ++k) {
+                    const uint32_t c = pos_ch[k];
+                    const uint32_t q = uint32_t(qof(A[c], origin[ob + c], delta[ob + c]));
+                    Pd[v][k] = double(std::fma(float(q), delta[ob + c], origin[ob + c]));
+                }
+            }
+            std::vector<std::array<uint32_t, 3>> tl;
+            for (uint32_t st : me.src_tri)
+                if (st != kNone) {
+                    const uint32_t* v = mesh.indices + 3ull * st;
+                    tl.push_back({loc[v[0]], loc[v[1]], loc[v[2]]});
+                }
+            cull_cone(Pd, tl, reinterpret_cast<float*>(B + off_cull + 16ull * m));
+        }
     }, 16);
     out.has_map = true;
     out.restarts = rs;
@@ -776,7 +847,8 @@ mc_status parse(const uint8_t* b, size_t nbytes, mc_layout* L) {
     std::memcpy(L->bits, b + 96, 16);
     std::memcpy(L->semantic, b + 112, 16);
     L->flags = get32(b + 60);
-    if (L->flags & ~1u) return MC_ERR_FORMAT;
+    L->off_cull = get64(b + 128);
+    if (L->flags & ~3u) return MC_ERR_FORMAT;
     if (L->codec != MC_CODEC_GTS && L->codec != MC_CODEC_GTS_REUSE && L->codec != MC_CODEC_BASIC) return MC_ERR_FORMAT;
     if (L->n < 1 || L->n > 16 || L->num_objects < 1 || L->v_max < 3 || L->v_max > 256 || L->t_max < 1 ||
         L->t_max > 256)
@@ -796,6 +868,10 @@ mc_status parse(const uint8_t* b, size_t nbytes, mc_layout* L) {
             ++c;
         }
     L->n_out = output_floats(L->n, L->semantic);
+    // the cull table lies between the object table and the records (FORMAT.md §1.5)
+    if ((L->flags & 2u) && ((L->off_cull & 15) || L->off_cull < L->off_obj + 8ull * L->n * L->num_objects ||
+                            L->off_cull + 16ull * L->num_meshlets > L->off_rec))
+        return MC_ERR_FORMAT;
     // the directory must stay inside the records section
     uint32_t d0 = get32(b + L->off_dir), dM = get32(b + L->off_dir + 4ull * L->num_meshlets);
     if (d0 != 0 || L->off_rec + 16ull * dM > nbytes) return MC_ERR_FORMAT;
@@ -850,6 +926,7 @@ mc_status mc_encode(const mc_mesh* mesh, const mc_encode_params* p, mc_blob** ou
     try {
         Encoder E(*mesh, p->max_vertices, p->max_triangles, p->codec, worker_count(p->num_threads),
                   (p->flags & MC_ENCODE_VARIABLE_WIDTHS) != 0);
+        E.cull = (p->flags & MC_ENCODE_CULL_CONES) != 0;
         mc_status st = E.run();
         if (st != MC_OK) return st;
         auto blob = std::make_unique<mc_blob>();
@@ -940,8 +1017,11 @@ mc_status mc_blob_extract(const void* bytes, size_t n, uint32_t first, uint32_t 
     *out = nullptr;
     const uint64_t d0 = get32(b + L.off_dir + 4ull * first), d1 = get32(b + L.off_dir + 4ull * (first + count));
     const uint64_t rec_bytes = 16 * (d1 - d0);
+    const bool cull = L.flags & 2u;
     const uint64_t off_dir = kHeaderBytes, off_obj = round16(off_dir + 4ull * (count + 1));
-    const uint64_t off_rec = round16(off_obj + 8ull * L.n * L.num_objects), total = off_rec + rec_bytes;
+    const uint64_t off_cull = cull ? round16(off_obj + 8ull * L.n * L.num_objects) : 0;
+    const uint64_t off_rec = cull ? round16(off_cull + 16ull * count) : round16(off_obj + 8ull * L.n * L.num_objects);
+    const uint64_t total = off_rec + rec_bytes;
     auto blob = std::make_unique<mc_blob>();
     if (!blob->allocate(total)) return MC_ERR_NOMEM;
     uint8_t* B = blob->bytes;
@@ -957,7 +1037,8 @@ mc_status mc_blob_extract(const void* bytes, size_t n, uint32_t first, uint32_t 
     }
     write_header(B, L.codec, L.n, count, L.num_objects, L.v_max, L.t_max, tv, ttp, tt, L.base_meshlet + first, bv, bt,
                  uint32_t(std::max<uint64_t>(maxrec, 16)), off_dir, off_obj, off_rec, total, L.bits, L.semantic,
-                 L.flags);
+                 L.flags, off_cull);
+    if (cull) std::memcpy(B + off_cull, b + L.off_cull + 16ull * first, 16ull * count);
     for (uint32_t m = 0; m <= count; ++m) put32(B + off_dir + 4ull * m, uint32_t(get32(b + L.off_dir + 4ull * (first + m)) - d0));
     std::memcpy(B + off_obj, b + L.off_obj, 8ull * L.n * L.num_objects);
     std::memcpy(B + off_rec, b + L.off_rec + 16 * d0, rec_bytes);
@@ -1013,13 +1094,17 @@ mc_status mc_blob_instance_range(const mc_blob* const* protos, uint32_t num_prot
         gm + M > 0xFFFFFFFFull)
         return MC_ERR_RANGE;
     const uint32_t n = L0.n;
+    const bool cull = L0.flags & 2u;
     const uint64_t off_dir = kHeaderBytes, off_obj = round16(off_dir + 4ull * (M + 1));
-    const uint64_t off_rec = round16(off_obj + 8ull * n * O), total = off_rec + rb;
+    const uint64_t off_cull = cull ? round16(off_obj + 8ull * n * O) : 0;
+    const uint64_t off_rec = cull ? round16(off_cull + 16ull * M) : round16(off_obj + 8ull * n * O);
+    const uint64_t total = off_rec + rb;
     auto blob = std::make_unique<mc_blob>();
     if (!blob->allocate(total)) return MC_ERR_NOMEM;
     uint8_t* B = blob->bytes;
     write_header(B, L0.codec, n, uint32_t(M), uint32_t(O), vmax, tmax, tv, ttp, tt, uint32_t(gm), uint32_t(gv),
-                 uint32_t(gt), uint32_t(maxrec), off_dir, off_obj, off_rec, total, L0.bits, L0.semantic, L0.flags);
+                 uint32_t(gt), uint32_t(maxrec), off_dir, off_obj, off_rec, total, L0.bits, L0.semantic, L0.flags,
+                 off_cull);
     // per-instance prefix sums, then fill instances in parallel
     std::vector<uint64_t> im(num_instances + 1, 0), io(num_instances + 1, 0), iv(num_instances + 1, 0),
         it(num_instances + 1, 0), ir(num_instances + 1, 0);
@@ -1048,6 +1133,8 @@ mc_status mc_blob_instance_range(const mc_blob* const* protos, uint32_t num_prot
                 }
         }
         std::memcpy(B + off_rec + ir[i], src + L.off_rec, L.total_bytes - L.off_rec);
+        // cones are translation invariant (the margin covers re-rounded origins)
+        if (cull) std::memcpy(B + off_cull + 16ull * im[i], src + L.off_cull, 16ull * L.num_meshlets);
         for (uint32_t m = 0; m < L.num_meshlets; ++m) {
             uint32_t d = get32(src + L.off_dir + 4ull * m);
             put32(B + off_dir + 4ull * (im[i] + m), uint32_t(ir[i] / 16 + d));

@@ -158,3 +158,63 @@ def test_product_encoder_variable_widths(mc, orc, codec):
             codes = q[r["vtx_base"]:r["vtx_base"] + r["V"]] - np.array(r["L"], np.int64)
             for c in range(n):
                 assert int(codes[:, c].max()).bit_length() == r["widths"][c] <= mesh.bits[c]
+
+
+def _backfacing_ok(orc, data, view_dirs):
+    """Brute force (FORMAT.md §7 soundness): every real triangle of every culled record
+    faces away from the view direction, in double precision from the decoded positions."""
+    from streams import read_records
+    err, errs, idx, q, f = orc.decode(data, want_q=False)
+    assert err == 0
+    info = orc.blob_info(data)
+    pos = f.reshape(-1, info.n_out)[:, :3].astype(np.float64)
+    recs = read_records(data)
+    culled = 0
+    for d in view_dirs:
+        e2, vis, c, *_ = orc.decode_culled(data, d, want_q=False, want_f=False)
+        assert e2 == 0
+        for r, v in zip(recs, vis):
+            if v:
+                continue
+            tb = r["tri_base"] - info.base_tri
+            t = idx[3 * tb:3 * (tb + r["Tp"])].reshape(-1, 3).astype(np.int64) - info.base_vtx
+            t = t[(t[:, 0] != t[:, 1]) & (t[:, 1] != t[:, 2]) & (t[:, 0] != t[:, 2])]
+            n = np.cross(pos[t[:, 1]] - pos[t[:, 0]], pos[t[:, 2]] - pos[t[:, 0]])
+            dots = n @ np.asarray(d, np.float64)
+            assert np.all(dots[np.linalg.norm(n, axis=1) > 0] > 0)
+            culled += 1
+    return culled / (len(view_dirs) * len(recs))
+
+
+def _dirs(seed, k=12):
+    rng = np.random.default_rng(seed)
+    d = rng.normal(size=(k, 3))
+    return (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
+
+
+@pytest.mark.parametrize("codec", [1, 2, 3])
+def test_product_cull_cones_sound(mc, orc, codec):
+    """mc_encode(cull_cones=True): the cones are sound (a culled meshlet is entirely
+    back-facing) and useful (a fair share of meshlets culls)."""
+    for mesh, lim in [(synth.displaced_sphere(24), (64, 126)), (synth.quad_grid(), (32, 32)),
+                      (synth.building(20, 4), (128, 256))]:
+        b = mc.mc_encode(mesh, *lim, codec, cull_cones=True)
+        data = np.array(b.bytes)
+        assert b.layout.flags & 2 and b.layout.off_cull > 0
+        frac = _backfacing_ok(orc, data, _dirs(codec))
+        assert frac > 0.04
+
+
+def test_cull_tables_survive_extract_and_instances(mc, orc):
+    scene = synth.city(num_instances=4, num_prototypes=2, k=10)
+    protos = [mc.mc_encode(p, 64, 126, 2, cull_cones=True) for p in scene.prototypes]
+    inst = mc.mc_blob_instance_range(protos, scene.instance_proto, scene.instance_offset, 1, 3)
+    data = np.array(inst.bytes)
+    assert inst.layout.flags & 2
+    _backfacing_ok(orc, data, _dirs(7, 6))                       # translated grids stay sound
+    b = mc.mc_encode(synth.displaced_sphere(20), 64, 126, 2, cull_cones=True)
+    full = np.array(b.bytes)
+    for f0, c in b.shard_ranges(3):
+        s = np.array(b.extract(f0, c).bytes)
+        d = _dirs(1, 1)[0]
+        assert np.array_equal(orc.decode_culled(s, d)[1], orc.decode_culled(full, d)[1][f0:f0 + c])
