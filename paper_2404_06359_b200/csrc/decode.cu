@@ -47,6 +47,9 @@
 #ifndef MC_GROUP8
 #define MC_GROUP8 0
 #endif
+#ifndef MC_ST_INTRIN
+#define MC_ST_INTRIN 0
+#endif
 #ifndef MC_BANK_PAD
 #define MC_BANK_PAD 1
 #endif
@@ -133,6 +136,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// Output stores.  MC_ST_CS: streaming (evict-first) stores — the outputs are never
+// re-read by this kernel.  MC_ST_INTRIN: CUDA's __stcs intrinsics instead of inline PTX
+// (lets the compiler keep the memory descriptor in uniform registers).
+#if MC_ST_INTRIN
+__device__ __forceinline__ void st_v4(uint32_t* p, uint4 v) {
+#if MC_ST_CS
+    __stcs(reinterpret_cast<uint4*>(p), v);
+#else
+    *reinterpret_cast<uint4*>(p) = v;
+#endif
+}
+__device__ __forceinline__ void st_u32(uint32_t* p, uint32_t v) {
+#if MC_ST_CS
+    __stcs(reinterpret_cast<unsigned int*>(p), v);
+#else
+    *p = v;
+#endif
+}
+#else
 #if MC_ST_CS
 #define MC_ST "st.global.cs"
 #else
@@ -145,6 +167,7 @@ __device__ __forceinline__ void st_v4(uint32_t* p, uint4 v) {
 __device__ __forceinline__ void st_u32(uint32_t* p, uint32_t v) {
     asm volatile(MC_ST ".u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+#endif
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z ^= z >> 30;
@@ -426,43 +449,44 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
 
         // ---------------- a3/a4/a5/a6: topology, one triangle per lane, G per step
         if (gl < 2) Nbuf[gl] = (uint8_t)gl;                                  // N[0], N[1]
-        uint32_t carry = 2u;                                                 // N[t+1] for group lane 0
+        // branch-free step: every lane computes, only the stores are predicated; N[t+1]
+        // and the pivot come from Nbuf after one group barrier (no neighbour shuffles)
         const uint32_t nsteps = (Tp + G - 1) / G;
         for (uint32_t j = 0; j < nsteps; ++j) {
             const uint32_t t = G * j + gl;
             const uint32_t wj = (G * j) >> 5;                                // flag word of this step
             const uint32_t bit = t & 31u;
             const bool active = t < Tp;
-            // a3: new-vertex index N[t+2] (w_0 := N[2] = 2)
-            uint32_t w = 2u;
+            const uint32_t lw = __shfl_sync(gm, lrw, wj, G);
+            const int p1 = __shfl_sync(gm, prev1, wj, G), p0 = __shfl_sync(gm, prev0, wj, G);
+            // a3: new-vertex index N[t+2] (w_0 := N[2] = 2); the byte read is always inside
+            // the group's shared memory (index masked to 8 bits), used only where valid
+            uint32_t w;
             if (CODEC == MC_CODEC_GTS) {
-                if (active && t >= 1u) w = BY[t - 1u];
+                const uint32_t bv = BY[(t - 1u) & 0xFFu];
+                w = t ? bv : 2u;
                 if (STATS && active && w >= V) e2 |= MC_DERR_INDEX;
             } else {
                 const uint32_t iw = __shfl_sync(gm, incw, wj, G);
                 const uint32_t c = __shfl_sync(gm, pc_excl, wj, G) + __popc(iw & (0xFFFFFFFFu >> (31u - bit)));   // inclusive c_t
-                if ((iw >> bit) & 1u) w = 2u + c;
-                else if (active && t >= 1u) {
-                    w = BY[t - c - 1u];                                      // location t+1-s, s = 2+c
-                    if (STATS && w >= V) e2 |= MC_DERR_REUSE;
-                }
+                const uint32_t rv = BY[(t - c - 1u) & 0xFFu];                // location t+1-s, s = 2+c
+                const bool inc = (iw >> bit) & 1u;
+                w = inc ? 2u + c : (t ? rv : 2u);
+                if (STATS && active && !inc && t && w >= V) e2 |= MC_DERR_REUSE;
             }
             if (active) Nbuf[t + 2u] = (uint8_t)w;
+            __syncwarp(gm);
             // a4: j(t) = max{k < t : f_k != f_t} by bit scan; earlier words
             // through the per-word last-R / last-L scans instead of a loop
-            const uint32_t lw = __shfl_sync(gm, lrw, wj, G);
-            const int p1 = __shfl_sync(gm, prev1, wj, G), p0 = __shfl_sync(gm, prev0, wj, G);
-            const uint32_t nprev_up = __shfl_up_sync(gm, w, 1, G);
-            const uint32_t nprev = gl ? nprev_up : carry;                    // N[t+1]
-            carry = __shfl_sync(gm, w, G - 1, G);
-            __syncwarp(gm);
+            const uint32_t nprev = Nbuf[t + 1u];                             // N[t+1]
+            const uint32_t f = (lw >> bit) & 1u;
+            const uint32_t x = (f ? ~lw : lw) & ((1u << bit) - 1u);
+            const int jj = x ? (int)(32u * wj) + 31 - __clz(x) : (f ? p0 : p1);
+            const uint32_t npiv = Nbuf[jj + 1];                              // N[j+1], N[0] if none
+            uint32_t a0 = f ? nprev : npiv, a1 = f ? npiv : nprev;           // a5 (FORMAT.md §2)
+            a0 = t ? a0 : 0u;
+            a1 = t ? a1 : 1u;
             if (active) {
-                const uint32_t f = (lw >> bit) & 1u;
-                const uint32_t x = (f ? ~lw : lw) & ((1u << bit) - 1u);
-                const int jj = x ? (int)(32u * wj) + 31 - __clz(x) : (f ? p0 : p1);
-                const uint32_t npiv = Nbuf[jj + 1];                          // N[j+1], N[0] if none
-                uint32_t a0 = f ? nprev : npiv, a1 = f ? npiv : nprev;       // a5 (FORMAT.md §2)
-                if (t == 0) { a0 = 0u; a1 = 1u; }
                 emit(t, a0, a1, w);                                          // a6
                 if (STATS) {
                     if (t > 0) ws.max_lb = max(ws.max_lb, (uint32_t)((int)t - jj));
