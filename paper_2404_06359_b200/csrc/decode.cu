@@ -196,11 +196,10 @@ __device__ __forceinline__ void group_store_words(uint32_t* dst, const uint32_t*
 __device__ __forceinline__ void oct_decode(float ex, float ey, float& ox, float& oy, float& oz) {
     const float ax = fabsf(ex), ay = fabsf(ey);
     const float z = __fsub_rn(__fsub_rn(1.0f, ax), ay);
-    float x = ex, y = ey;
-    if (z < 0.0f) {
-        x = __fmul_rn(__fsub_rn(1.0f, ay), ex >= 0.0f ? 1.0f : -1.0f);
-        y = __fmul_rn(__fsub_rn(1.0f, ax), ey >= 0.0f ? 1.0f : -1.0f);
-    }
+    // fold (z < 0) by selects, no branch
+    const float fx = __fmul_rn(__fsub_rn(1.0f, ay), ex >= 0.0f ? 1.0f : -1.0f);
+    const float fy = __fmul_rn(__fsub_rn(1.0f, ax), ey >= 0.0f ? 1.0f : -1.0f);
+    const float x = z < 0.0f ? fx : ex, y = z < 0.0f ? fy : ey;
     const float s2 = __fmaf_rn(z, z, __fmaf_rn(y, y, __fmul_rn(x, x)));
     const float r = __fsqrt_rn(s2);
     const float inv = __frcp_rn(r);
@@ -481,7 +480,9 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
             const uint32_t nprev = Nbuf[t + 1u];                             // N[t+1]
             const uint32_t f = (lw >> bit) & 1u;
             const uint32_t x = (f ? ~lw : lw) & ((1u << bit) - 1u);
-            const int jj = x ? (int)(32u * wj) + 31 - __clz(x) : (f ? p0 : p1);
+            const int hi = (int)(32u * wj) + 31 - __clz(x);                  // computed even for x = 0
+            const int pw = f ? p0 : p1;
+            const int jj = x ? hi : pw;                                      // select, no branch
             const uint32_t npiv = Nbuf[jj + 1];                              // N[j+1], N[0] if none
             uint32_t a0 = f ? nprev : npiv, a1 = f ? npiv : nprev;           // a5 (FORMAT.md §2)
             a0 = t ? a0 : 0u;
