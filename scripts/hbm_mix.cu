@@ -88,7 +88,7 @@ __global__ void tma_store(const uint4* __restrict__ src, uint8_t* __restrict__ d
     if (acc == 0x12345678u) out[0] = acc;
 }
 
-int main() {
+int main1() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const size_t src_bytes = 1107328176ull & ~65535ull;   // cfg4 compressed bytes per GPU
@@ -142,4 +142,77 @@ int main() {
         });
     }
     return 0;
+}
+
+// ---- second probe: read 1 : write 3 through shared memory, stored either with plain
+// coalesced 128-bit stores or with TMA bulk stores (cp.async.bulk.global.shared::cta),
+// double-buffered; the structure of a decoder that stages its outputs.
+template <bool TMA>
+__global__ void __launch_bounds__(256) mix_smem(const uint4* __restrict__ src, uint4* __restrict__ dst, size_t nsrc) {
+    constexpr int kIn = 256;                       // uint4 read per CTA iteration (4 KB)
+    constexpr int kOut = 3 * kIn;                  // uint4 written (12 KB)
+    __shared__ __align__(128) uint4 tile[2][kOut];
+    const size_t iters = nsrc / kIn;
+    int k = 0;
+    for (size_t it = blockIdx.x; it < iters; it += gridDim.x, ++k) {
+        uint4* t = tile[k & 1];
+        if (TMA && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();
+        const uint4 v = src[it * kIn + threadIdx.x];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) t[r * kIn + threadIdx.x] = make_uint4(v.x + r, v.y, v.z, v.w);
+        if (TMA) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + it * kOut),
+                             "r"((uint32_t)__cvta_generic_to_shared(t)), "r"((uint32_t)(kOut * 16))
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        } else {
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < 3; ++r) dst[it * kOut + r * kIn + threadIdx.x] = t[r * kIn + threadIdx.x];
+        }
+    }
+    if (TMA && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+int main2() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const size_t src_bytes = 1107328176ull & ~65535ull;
+    const size_t n = src_bytes / 16;
+    uint4 *src, *dst;
+    cudaMalloc(&src, src_bytes);
+    cudaMalloc(&dst, src_bytes * 3 + 65536);
+    cudaMemset(src, 1, src_bytes);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int bps : {2, 3, 4, 6, 8}) {
+        for (int tma = 0; tma < 2; ++tma) {
+            auto launch = [&] {
+                if (tma) mix_smem<true><<<sms * bps, 256>>>(src, dst, n);
+                else mix_smem<false><<<sms * bps, 256>>>(src, dst, n);
+            };
+            for (int i = 0; i < 3; ++i) launch();
+            cudaEventRecord(e0);
+            for (int i = 0; i < 20; ++i) launch();
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            printf("{\"case\": \"smem-staged read1:write3 %s grid=%dx%d\", \"GB/s\": %.1f, \"err\": \"%s\"}\n",
+                   tma ? "TMA-store" : "STG.128", sms, bps, 4.0 * src_bytes * 20 / (ms * 1e-3) / 1e9,
+                   cudaGetErrorString(cudaGetLastError()));
+        }
+    }
+    return 0;
+}
+
+int main(int argc, char** argv) {
+    if (argc > 1 && argv[1][0] == '2') return main2();
+    return main1();
 }
