@@ -533,11 +533,15 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
                         og[c] = __ldg(ot + NCH + c);
                     }
                 }
-                uint32_t bw[NCH];                                            // code widths
+                uint32_t bo[NCH], bm[NCH];                                   // code offset, mask
+                uint32_t off = 0;
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) {
                     Lc[c] = R[4 + c];
-                    bw[c] = B16 ? 16u : (VWK ? (uint32_t)WB[c] : (uint32_t)P.bits[c]);
+                    const uint32_t bw = B16 ? 16u : (VWK ? (uint32_t)WB[c] : (uint32_t)P.bits[c]);
+                    bo[c] = off;
+                    bm[c] = bw >= 32u ? 0xFFFFFFFFu : ((1u << bw) - 1u);
+                    off += bw;
                 }
                 for (uint32_t v = gl; v < V; v += G) {
                     uint32_t qv[NCH];
@@ -546,19 +550,15 @@ __global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(cons
 #pragma unroll
                         for (int c = 0; c < NCH; ++c) qv[c] = Lc[c] + H[c];   // q = L_c + code
                     } else {
-                        // little-endian bit reader over the vertex record (FORMAT.md §1.4)
+                        // little-endian bit string (FORMAT.md §1.4): the code of channel c
+                        // is the bw[c]-bit field at bit v·S + o_c, read as a funnel shift of
+                        // the two words that hold it (independent per channel, no branches)
                         const uint32_t bit0 = v * Sm;
-                        const uint32_t* wp = AT + (bit0 >> 5);
-                        uint64_t acc = (uint64_t)(wp[0] >> (bit0 & 31u));
-                        uint32_t avail = 32u - (bit0 & 31u);
-                        ++wp;
 #pragma unroll
                         for (int c = 0; c < NCH; ++c) {
-                            const uint32_t bb = bw[c];
-                            if (avail < bb) { acc |= (uint64_t)(*wp++) << avail; avail += 32u; }
-                            qv[c] = Lc[c] + ((uint32_t)acc & ((1u << bb) - 1u));
-                            acc >>= bb;
-                            avail -= bb;
+                            const uint32_t pb = bit0 + bo[c];
+                            const uint32_t* wp = AT + (pb >> 5);
+                            qv[c] = Lc[c] + (__funnelshift_r(wp[0], wp[1], pb & 31u) & bm[c]);
                         }
                     }
                     if (want_q) {
