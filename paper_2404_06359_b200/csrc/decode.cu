@@ -224,8 +224,15 @@ struct WarpStats {
 // with each record's widths (FORMAT.md VW).  B16 (AM == 0): every channel is 16 bits wide (the paper's
 // b = 16) so codes are read as aligned halfwords.  NCH == 0: generic
 // runtime layout (any n <= 16, widths 1..24, any octahedral placement).
+// Register budget: 3 CTAs x 8 warps per SM is the measured optimum (profiles/experiments);
+// variants that would otherwise take more than 80 registers are capped to keep 3 CTAs/SM.
+template <int NCH, int AM>
+constexpr int min_blocks() {
+    return MC_MIN_BLOCKS > 1 ? MC_MIN_BLOCKS : ((NCH == 7 && AM == 0) ? 1 : 3);
+}
+
 template <int G, int CODEC, bool STATS, int NCH, int OCT0, int AM>
-__global__ void __launch_bounds__(kThreads, MC_MIN_BLOCKS) mc_decode_kernel(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_kernel(const __grid_constant__ Params P) {
     static_assert(G == 8 || G == 16 || G == 32, "group size");
     constexpr bool B16 = AM == 0, VWK = AM == 2;
     constexpr int NG = 32 / G;                      // groups (meshlets in flight) per warp
