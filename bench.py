@@ -47,6 +47,8 @@ WORKLOADS = {
     "cfg3_sphere": dict(desc="displaced cube-sphere 12*913^2 = 10.0M tris, pos3+oct2+uv2 @16b", vmax=64, tmax=126),
     "cfg4_city": dict(desc="instanced city, 1000 instances x 99,372 tris per GPU, pos3+oct2+uv2 @16b",
                       vmax=64, tmax=126),
+    "cfg3_sphere_nrm8": dict(desc="cfg3 sphere with raw normals: pos3+nrm3+uv2 @16b (the paper's 8 attributes)",
+                             vmax=64, tmax=126),
 }
 
 
@@ -72,7 +74,8 @@ def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: 
         return blob, meta
     mesh = {"cfg1_grid": lambda: synth.quad_grid(32, 32),
             "cfg2_torus": lambda: synth.torus(1000, 500),
-            "cfg3_sphere": lambda: synth.displaced_sphere(913)}[workload]()
+            "cfg3_sphere": lambda: synth.displaced_sphere(913),
+            "cfg3_sphere_nrm8": lambda: synth.displaced_sphere(913, oct_normals=False)}[workload]()
     blob = mc.mc_encode(mesh, w["vmax"], w["tmax"], codec, variable_widths=vw, cull_cones=cull)
     meta = {"restarts_per_meshlet": round(blob.encode_stats()["restarts"] / max(1, blob.layout.num_meshlets), 3)}
     if world > 1:   # strong-sharded replicas of the single mesh

@@ -20,6 +20,9 @@
  *    mc_stats.error_bits (FORMAT.md §5) — the kernel never traps and never
  *    reads or writes outside the blob and the record's own output ranges.
  *  - Every function is thread-safe; mc_blob objects are immutable once built.
+ *  - Each decode launch claims records from a block of device counters in the library
+ *    (rotating over 64 blocks, zeroed on the launch's own stream): at most 64 decode
+ *    launches may be in flight at once across all streams of a process.
  */
 #ifndef MC_H
 #define MC_H

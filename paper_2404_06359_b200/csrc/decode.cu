@@ -47,6 +47,9 @@
 #ifndef MC_GROUP8
 #define MC_GROUP8 0
 #endif
+#ifndef MC_DYNAMIC
+#define MC_DYNAMIC 128   // interleaved claim streams (0 = static grid stride)
+#endif
 #ifndef MC_ST_INTRIN
 #define MC_ST_INTRIN 0
 #endif
@@ -79,6 +82,7 @@ struct Params {
     uint32_t hdr_words;        // record header words (16 + 4n [+ n with VW] rounded to 16) / 4
     uint32_t vw;               // FORMAT.md VW: per-record attribute widths w_c after L_c
     const uint4* list;         // culled decode (FORMAT.md §7): visible records {m, VB, TB, 0}, or null
+    uint32_t* ctr;             // MC_DYNAMIC: this launch's claim counters (device, zeroed)
     const uint32_t* list_count;// device count of list entries
     uint32_t buf_words;        // per-buffer words (max_rec/4 + 4)
     uint32_t vtx_stage_words;  // vmax*n_out + 8 for the generic layout, else 0
@@ -214,6 +218,14 @@ struct WarpStats {
 };
 
 
+#if MC_DYNAMIC
+// Position counters for the claim streams: kCounterBlocks blocks of MC_DYNAMIC counters,
+// one block per launch, rotating (up to kCounterBlocks decode launches may be in flight
+// at once across streams; each launch zeroes its block on its own stream first).
+constexpr uint32_t kCounterBlocks = 64;
+__device__ uint32_t g_position_counters[kCounterBlocks * MC_DYNAMIC];
+#endif
+
 // ------------------------------------------------------------------ the kernel
 // G: lanes per meshlet (32 = one warp per meshlet, 16 = two meshlets per warp, each
 // half-warp an independent "group" with its own staging buffers, barriers and lane
@@ -258,18 +270,26 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
     uint8_t* Nbuf = reinterpret_cast<uint8_t*>(misc + 40);            // N[0..T'+1], 272 B
     uint32_t* lbase = misc + 112;                                     // list mode: VB[2], TB[2] per buffer
 
-    const uint32_t ngroups = gridDim.x * wpc * NG;
     const uint32_t gg = blockIdx.x * wpc * NG + gslot;
-#if MC_CONTIG
-    // contiguous record range per group
-    const uint32_t per = (P.end - P.first + ngroups - 1) / ngroups;
-    uint32_t m = P.first + min(gg * per, P.end - P.first);
-    const uint32_t mstop = min(P.end, m + per), mstep = 1;
+    // Sequence positions (record ids, or entries of a culled decode's visible list,
+    // FORMAT.md §7) are claimed per group from MC_DYNAMIC interleaved counters (claims stay
+    // in global order, so neighbouring records are decoded at about the same time, and
+    // groups on slower SMs simply claim fewer records; the static grid stride left up to
+    // 35% of the time on an imbalanced tail, profiles/experiments), or, with
+    // MC_DYNAMIC = 0, by a static grid stride.
+    const uint32_t base0 = P.list ? 0u : P.first;
+    const uint32_t mstop = P.list ? min(*P.list_count, P.end) : P.end;
+#if MC_DYNAMIC
+    // MC_DYNAMIC interleaved streams: positions s, s + NS, s + 2 NS, ... are handed out by
+    // counter s (= group id mod NS), so claims stay in global order (neighbouring records
+    // decoded at about the same time) while each counter sees 1/NS of the atomics
+    constexpr uint32_t NS = MC_DYNAMIC;
+    const uint32_t stream = gg % NS;
+    auto grab = [&]() -> uint32_t { return base0 + stream + NS * atomicAdd(P.ctr + stream, 1u); };
 #else
-    // grid stride: neighbouring groups decode neighbouring records (list mode: neighbouring
-    // entries of the visible-record list of a culled decode, FORMAT.md §7)
-    uint32_t m = P.list ? gg : P.first + gg;
-    const uint32_t mstop = P.list ? min(*P.list_count, P.end) : P.end, mstep = ngroups;
+    const uint32_t ngroups = gridDim.x * wpc * NG;
+    uint32_t grabbed = 0;
+    auto grab = [&]() -> uint32_t { return base0 + gg + (grabbed++) * ngroups; };
 #endif
     // record id of sequence position i (identity, or the culled decode's visible list)
     auto rid = [&](uint32_t i) -> uint32_t { return P.list ? __ldg(&P.list[i].x) : i; };
@@ -303,28 +323,47 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
     };
 
     uint32_t nd0 = 0, nd1 = 0;   // directory entries of the record after next (prefetched)
-    if (m < mstop && gl == 0) {
-        const uint32_t r0 = rid(m);
-        issue(__ldg(P.dir + r0), __ldg(P.dir + r0 + 1), 0, m);
-        if (m + mstep < mstop) {
-            const uint32_t r1 = rid(m + mstep);
+    uint32_t m = 0, mnext = 0, m2 = 0;   // current, next, after-next positions (lane 0 of the group)
+    if (gl == 0) {
+        m = grab();
+        mnext = grab();
+        if (m < mstop) {
+            const uint32_t r0 = rid(m);
+            issue(__ldg(P.dir + r0), __ldg(P.dir + r0 + 1), 0, m);
+        }
+        if (mnext < mstop) {
+            const uint32_t r1 = rid(mnext);
             nd0 = __ldg(P.dir + r1);
             nd1 = __ldg(P.dir + r1 + 1);
         }
     }
+    uint32_t* pcast = misc + 6;          // the group's current position, broadcast through smem
 
     WarpStats ws;
-    uint32_t k = 0;
-    for (; m < mstop; m += mstep, ++k) {
+    // advance the group's positions (lane 0); runs on every path, `continue` included
+    auto advance = [&]() {
+        if (gl == 0) {
+            m = mnext;
+            mnext = m2;
+        }
+    };
+    for (uint32_t k = 0;; ++k, advance()) {
+        if (gl == 0) pcast[0] = m;
+        __syncwarp(gm);
+        m = pcast[0];                        // group-uniform
+        if (m >= mstop) break;
         const int b = k & 1;
-        const uint32_t mnext = m + mstep;
-        if (gl == 0 && mnext < mstop) {
-            issue(nd0, nd1, b ^ 1, mnext);
-            const uint32_t m2 = mnext + mstep;
-            if (m2 < mstop) {
-                const uint32_t r2 = rid(m2);
-                nd0 = __ldg(P.dir + r2);
-                nd1 = __ldg(P.dir + r2 + 1);
+        if (gl == 0) {
+            if (mnext < mstop) {
+                issue(nd0, nd1, b ^ 1, mnext);
+                m2 = grab();
+                if (m2 < mstop) {
+                    const uint32_t r2 = rid(m2);
+                    nd0 = __ldg(P.dir + r2);
+                    nd1 = __ldg(P.dir + r2 + 1);
+                }
+            } else {
+                m2 = mnext;                  // stays past the end (positions are monotone)
             }
         }
         mbar_wait(&bars[b], (k >> 1) & 1);
@@ -902,11 +941,23 @@ mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
         if (bps < 1) return MC_ERR_LIMITS;
         bps_cache[wpc][bucket] = bps;
     }
+    Params PL = P;
+#if MC_DYNAMIC
+    {
+        static uint32_t* slots = nullptr;
+        static uint32_t seq = 0;
+        std::lock_guard<std::mutex> g(mu);
+        if (!slots && cudaGetSymbolAddress(reinterpret_cast<void**>(&slots), g_position_counters) != cudaSuccess)
+            return MC_ERR_CUDA;
+        PL.ctr = slots + MC_DYNAMIC * (seq++ % kCounterBlocks);
+        if (cudaMemsetAsync(PL.ctr, 0, 4 * MC_DYNAMIC, s) != cudaSuccess) return MC_ERR_CUDA;
+    }
+#endif
     const uint32_t count = P.end - P.first;
     const uint64_t want = (count + wpc * NG - 1) / (wpc * NG);
     const uint64_t cap = (uint64_t)sms * std::min(bps, MC_MAX_CTAS_PER_SM);
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
-    kern<<<grid, 32 * wpc, smem, s>>>(P);
+    kern<<<grid, 32 * wpc, smem, s>>>(PL);
     return cudaGetLastError() == cudaSuccess ? MC_OK : MC_ERR_CUDA;
 }
 
