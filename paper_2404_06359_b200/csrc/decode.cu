@@ -27,7 +27,15 @@
 //
 // No tensor cores: the path is integer bit manipulation plus one FMA per
 // channel, bound by HBM bandwidth.  No --use_fast_math.
-// Compile-time knobs (MC_*) below exist for A/B experiments (scripts/build_variants.sh).
+// Compile-time tuning knobs (defaults are the measured optimum on B200, A/B tables in
+// profiles/experiments; scripts/build_variants.sh builds alternatives):
+//   MC_MIN_BLOCKS       __launch_bounds__ min blocks (default: 3 CTAs/SM, 80-register cap
+//                       on every variant except the hot b = 16 octahedral layout)
+//   MC_MAX_CTAS_PER_SM  cap on resident CTAs per SM used to size the persistent grid
+//   MC_GROUP16_TMAX     two meshlets per warp (16-lane groups) when T~ <= this
+//   MC_DYNAMIC          interleaved claim counters (0 = static grid stride)
+//   MC_ST_CS            streaming (.cs) output stores
+//   MC_BANK_PAD         group smem stride = 16 (mod 32) words
 #include "../../include/mc.h"
 
 #include <cuda_runtime.h>
@@ -44,20 +52,11 @@
 #ifndef MC_GROUP16_TMAX
 #define MC_GROUP16_TMAX 128
 #endif
-#ifndef MC_GROUP8
-#define MC_GROUP8 0
-#endif
 #ifndef MC_DYNAMIC
 #define MC_DYNAMIC 128   // interleaved claim streams (0 = static grid stride)
 #endif
-#ifndef MC_ST_INTRIN
-#define MC_ST_INTRIN 0
-#endif
 #ifndef MC_BANK_PAD
 #define MC_BANK_PAD 1
-#endif
-#ifndef MC_CONTIG
-#define MC_CONTIG 0
 #endif
 #ifndef MC_MAX_CTAS_PER_SM
 #define MC_MAX_CTAS_PER_SM 64
@@ -141,24 +140,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 // Output stores.  MC_ST_CS: streaming (evict-first) stores — the outputs are never
-// re-read by this kernel.  MC_ST_INTRIN: CUDA's __stcs intrinsics instead of inline PTX
-// (lets the compiler keep the memory descriptor in uniform registers).
-#if MC_ST_INTRIN
-__device__ __forceinline__ void st_v4(uint32_t* p, uint4 v) {
-#if MC_ST_CS
-    __stcs(reinterpret_cast<uint4*>(p), v);
-#else
-    *reinterpret_cast<uint4*>(p) = v;
-#endif
-}
-__device__ __forceinline__ void st_u32(uint32_t* p, uint32_t v) {
-#if MC_ST_CS
-    __stcs(reinterpret_cast<unsigned int*>(p), v);
-#else
-    *p = v;
-#endif
-}
-#else
+// re-read by this kernel (+1.5-2.5% on cfg4).
 #if MC_ST_CS
 #define MC_ST "st.global.cs"
 #else
@@ -171,7 +153,6 @@ __device__ __forceinline__ void st_v4(uint32_t* p, uint4 v) {
 __device__ __forceinline__ void st_u32(uint32_t* p, uint32_t v) {
     asm volatile(MC_ST ".u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-#endif
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z ^= z >> 30;
@@ -653,19 +634,16 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
                 const uint32_t fphase = want_f ? ((uint32_t)(reinterpret_cast<uintptr_t>(fdst) >> 2) & 3u) : 0u;
                 uint32_t* vst = vtx_stage + fphase;
                 for (uint32_t v = gl; v < V; v += G) {
-                    const uint32_t bit0 = v * Sm;
-                    const uint32_t* wp = AT + (bit0 >> 5);
-                    uint64_t acc = (uint64_t)(wp[0] >> (bit0 & 31u));
-                    uint32_t avail = 32u - (bit0 & 31u);
-                    ++wp;
+                    uint32_t pb = v * Sm;                                    // bit of the current code
                     uint32_t* qd = want_q ? P.qout + (size_t)P.n * (vpos + v) : nullptr;
                     float xprev = 0.0f;
                     for (uint32_t c = 0; c < P.n; ++c) {
+                        // FORMAT.md §1.4 bit string: funnel shift of the two words holding the code
                         const uint32_t bb = VWK ? (uint32_t)WB[c] : (uint32_t)P.bits[c];
-                        if (avail < bb) { acc |= (uint64_t)(*wp++) << avail; avail += 32u; }
-                        const uint32_t q = R[4 + c] + ((uint32_t)acc & ((1u << bb) - 1u));
-                        acc >>= bb;
-                        avail -= bb;
+                        const uint32_t* wp = AT + (pb >> 5);
+                        const uint32_t code = __funnelshift_r(wp[0], wp[1], pb & 31u) & ((1u << bb) - 1u);
+                        const uint32_t q = R[4 + c] + code;
+                        pb += bb;
                         if (want_q) {
                             st_u32(qd + c, q);
                             if (STATS) ws.cs_q += mix64((((uint64_t)P.n * (vtx_base + v) + c) << 32) | q);
@@ -965,9 +943,6 @@ mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
 // MC_GROUP16_TMAX decoded triangles, else one meshlet per warp (G = 32)
 template <int CODEC, bool STATS, int NCH, int OCT0, int AM>
 mc_status launch_t(const Params& P, size_t grp_smem, cudaStream_t s) {
-#if MC_GROUP8
-    if (P.tmax <= MC_GROUP16_TMAX) return launch_g<8, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
-#endif
     if (P.tmax <= MC_GROUP16_TMAX) return launch_g<16, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
     return launch_g<32, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
 }
