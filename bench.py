@@ -348,7 +348,7 @@ def run_ours(args, rank, world, local_rank):
         ke = max(1, min(args.steps, args.e2e_steps))
         for _ in range(1):
             mc.mc_decode_host(L, h_blob, db.d_blob, h_idx, db.indices, h_v, db.vertices, flags=db.index_flags,
-                              stream=stream)
+                              stream=stream, chunks=args.e2e_chunks)
         torch.cuda.synchronize(dev)
         if dist:
             dist.barrier()
@@ -356,7 +356,7 @@ def run_ours(args, rank, world, local_rank):
         e0.record(stream)
         for _ in range(ke):
             mc.mc_decode_host(L, h_blob, db.d_blob, h_idx, db.indices, h_v, db.vertices, flags=db.index_flags,
-                              stream=stream)
+                              stream=stream, chunks=args.e2e_chunks)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -364,7 +364,9 @@ def run_ours(args, rank, world, local_rank):
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e = {"value": tri_all * ke / (float(et[0]) * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(data.nbytes), "d2h_bytes_per_step": int(4 * idx_words + 4 * L.n_out * L.total_v),
-               "steps": ke, "path": "mc_decode_host (pinned host blob -> HBM -> decode -> pinned host outputs)"}
+               "steps": ke, "chunks": args.e2e_chunks,
+               "path": "mc_decode_host (pinned host blob -> HBM -> decode -> pinned host outputs; "
+                       "chunks >= 2: H2D / decode / D2H pipelined over record ranges)"}
 
     if rank != 0:
         if dist:
@@ -427,6 +429,7 @@ def main():
     ap.add_argument("--instances", type=int, default=1000, help="cfg4 instances per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-chunks", type=int, default=32, help="mc_decode_host pipeline depth (0/1 = serial)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -226,8 +226,24 @@ mc_status mc_decode_culled(const mc_decode_args *args, const float *view_dir, vo
 mc_status mc_stats_reset(mc_stats *d_stats, void *stream);
 
 /* End-to-end decode from HOST buffers: H2D of the blob, decode, D2H of the
- * outputs, all enqueued on `stream` (host buffers should be pinned for overlap).
- * Device buffers are caller-owned scratch of the sizes mc_decode_args states. */
+ * outputs, ordered on `stream` (host buffers must be pinned for the copies to be
+ * asynchronous).  Device buffers are caller-owned scratch of the sizes
+ * mc_decode_args states.
+ *
+ * chunks <= 1: one H2D of the whole blob, one decode, one D2H per output, all on
+ * `stream`.  chunks >= 2: software pipeline over PCIe — the header, directory,
+ * object and cull tables go first, then the record section in `chunks` contiguous
+ * byte-balanced record ranges; chunk c's H2D (library-owned copy-in stream), decode
+ * (on `stream`) and D2H (library-owned copy-out stream) are chained by events, so
+ * chunk c+1 is copied in and chunk c-1 copied out while chunk c decodes (PCIe is
+ * full duplex: the step costs about max(H2D, D2H) instead of their sum).  The call
+ * stays asynchronous: the copy streams first wait for work already on `stream`, and
+ * `stream` waits for the last copy-out before anything enqueued after the call.
+ * Requires records whose output ranges follow record order (vtx_base and tri_base
+ * non-decreasing, as every blob this library writes has them): each chunk copies
+ * back the output span between its first record's bases and the next chunk's; the
+ * call checks the chunk boundaries and otherwise falls back to chunks = 1.
+ * The library streams/events are created once per device on first use. */
 typedef struct {
     const mc_layout *layout;
     const void *h_blob;        /* host: total_bytes                                       */
@@ -239,11 +255,12 @@ typedef struct {
     float *d_vertices;         /* device scratch or NULL (NULL iff h_vertices NULL)       */
     uint32_t *d_quantized;     /* device scratch or NULL                                   */
     uint32_t flags;
+    uint32_t chunks;           /* pipeline depth (0/1 = serial, capped at 64)              */
 } mc_host_decode_args;
 mc_status mc_decode_host(const mc_host_decode_args *args, void *stream);
 
 const char *mc_status_str(mc_status s);
-uint32_t mc_abi_version(void);   /* 2 (mc_encode_params.flags, mc_layout.flags) */
+uint32_t mc_abi_version(void);   /* 3 (mc_encode_params.flags, mc_layout.flags, mc_host_decode_args.chunks) */
 
 #ifdef __cplusplus
 }

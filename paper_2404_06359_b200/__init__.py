@@ -22,7 +22,7 @@ LIB_PATH = _build.LIB
 MC_CODEC_GTS, MC_CODEC_GTS_REUSE, MC_CODEC_BASIC = 1, 2, 3
 MC_DECODE_BLOB_LOCAL_INDICES, MC_DECODE_INDEX_LOCAL_U8X4 = 1, 2
 MC_ENCODE_VARIABLE_WIDTHS, MC_ENCODE_CULL_CONES = 1, 2
-ABI_VERSION = 2
+ABI_VERSION = 3
 MC_DERR_RECORD, MC_DERR_COUNTS, MC_DERR_INDEX, MC_DERR_REUSE, MC_DERR_OBJECT = 1, 2, 4, 8, 16
 
 
@@ -62,7 +62,7 @@ class mc_host_decode_args(ctypes.Structure):
     _fields_ = [("layout", ctypes.POINTER(mc_layout)), ("h_blob", ctypes.c_void_p), ("d_blob", ctypes.c_void_p),
                 ("h_indices", ctypes.c_void_p), ("h_vertices", ctypes.c_void_p), ("h_quantized", ctypes.c_void_p),
                 ("d_indices", ctypes.c_void_p), ("d_vertices", ctypes.c_void_p), ("d_quantized", ctypes.c_void_p),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("chunks", ctypes.c_uint32)]
 
 
 class mc_stats(ctypes.Structure):
@@ -304,13 +304,16 @@ def read_stats(d_stats) -> dict:
 
 
 def mc_decode_host(layout: mc_layout, h_blob, d_blob, h_indices, d_indices, h_vertices=None, d_vertices=None,
-                   h_quantized=None, d_quantized=None, flags: int = 0, stream=None):
-    """End-to-end decode from host tensors (pinned for overlap): H2D, decode, D2H on `stream`."""
+                   h_quantized=None, d_quantized=None, flags: int = 0, stream=None, chunks: int = 32):
+    """End-to-end decode from host tensors (pinned for overlap): H2D, decode, D2H ordered on
+    `stream`; chunks >= 2 pipelines them over byte-balanced record ranges (include/mc.h)."""
+    _check_sizes(layout, d_blob, d_indices, d_vertices, d_quantized, flags)
+    _check_sizes(layout, h_blob, h_indices, h_vertices, h_quantized, flags)
     a = mc_host_decode_args(ctypes.pointer(layout), h_blob.data_ptr(), d_blob.data_ptr(), h_indices.data_ptr(),
                             None if h_vertices is None else h_vertices.data_ptr(),
                             None if h_quantized is None else h_quantized.data_ptr(), d_indices.data_ptr(),
                             None if d_vertices is None else d_vertices.data_ptr(),
-                            None if d_quantized is None else d_quantized.data_ptr(), flags)
+                            None if d_quantized is None else d_quantized.data_ptr(), flags, chunks)
     _check(lib().mc_decode_host(ctypes.byref(a), _stream_handle(stream)), "mc_decode_host")
 
 

@@ -41,7 +41,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #ifndef MC_MIN_BLOCKS
 #define MC_MIN_BLOCKS 1
@@ -1014,6 +1016,76 @@ mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s, const ui
     return dispatch_codec(L.codec, st != nullptr, lay, am, P, smem, s);
 }
 
+
+// ------------------------------------------------------------------ mc_decode_host pipeline
+// Chunk c of a pipelined host decode: records [first, next.first), record bytes from
+// rec_off, outputs from the first record's bases (the last entry is the end sentinel).
+struct HostChunk {
+    uint32_t first;
+    uint64_t rec_off;   // byte offset inside the records section (16 * dir[first])
+    uint32_t vtx, tri;  // vtx_base / tri_base of record `first` (end: base + total)
+};
+
+// Byte-balanced chunk boundaries by binary search over the directory (O(chunks log M),
+// no pass over the records), bases read from the boundary records' headers.  Returns
+// fewer than two entries when the blob does not meet the ordering precondition
+// (include/mc.h), which selects the serial path.
+std::vector<HostChunk> plan_host_chunks(const mc_layout& L, const uint8_t* hb, uint32_t chunks) {
+    std::vector<HostChunk> ch;
+    const uint32_t M = L.num_meshlets;
+    const uint32_t* dir = reinterpret_cast<const uint32_t*>(hb + L.off_dir);
+    const uint64_t rec_bytes = L.total_bytes - L.off_rec;
+    if (16ull * dir[M] > rec_bytes) return ch;
+    chunks = std::min(chunks, M);
+    for (uint32_t c = 0; c < chunks; ++c) {
+        const uint64_t target = (uint64_t)dir[M] * c / chunks;   // in 16-B units
+        const uint32_t m = c == 0 ? 0u : (uint32_t)(std::lower_bound(dir, dir + M, (uint32_t)target) - dir);
+        if (!ch.empty() && m <= ch.back().first) continue;      // empty chunk (one huge record)
+        const uint32_t* rh = reinterpret_cast<const uint32_t*>(hb + L.off_rec + 16ull * dir[m]);
+        ch.push_back({m, 16ull * dir[m], rh[0], rh[1]});
+    }
+    ch.push_back({M, 16ull * dir[M], L.base_vtx + L.total_v, L.base_tri + L.total_tp});
+    for (size_t c = 0; c < ch.size(); ++c) {   // boundary bases ascending inside the output ranges
+        const bool bad = ch[c].vtx < L.base_vtx || ch[c].tri < L.base_tri ||
+                         (uint64_t)ch[c].vtx > (uint64_t)L.base_vtx + L.total_v ||
+                         (uint64_t)ch[c].tri > (uint64_t)L.base_tri + L.total_tp ||
+                         (c > 0 && (ch[c].vtx < ch[c - 1].vtx || ch[c].tri < ch[c - 1].tri)) ||
+                         (c == 0 && (ch[0].vtx != L.base_vtx || ch[0].tri != L.base_tri));
+        if (bad) return {};
+    }
+    return ch;
+}
+
+// Library-owned copy streams and events of the pipelined host decode, one set per device.
+constexpr int kMaxDevices = 64;
+struct PipeRes {
+    std::mutex mu;
+    cudaStream_t in = nullptr, out = nullptr;
+    cudaEvent_t start = nullptr, done = nullptr, in_done[64] = {}, dec_done[64] = {};
+};
+PipeRes* pipe_res() {
+    static PipeRes res[kMaxDevices];
+    static std::mutex mu;
+    static bool ready[kMaxDevices] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+    std::lock_guard<std::mutex> g(mu);
+    PipeRes& r = res[dev];
+    if (!ready[dev]) {
+        const unsigned ef = cudaEventDisableTiming;
+        if (cudaStreamCreateWithFlags(&r.in, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&r.out, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&r.start, ef) != cudaSuccess || cudaEventCreateWithFlags(&r.done, ef) != cudaSuccess)
+            return nullptr;
+        for (int i = 0; i < 64; ++i)
+            if (cudaEventCreateWithFlags(&r.in_done[i], ef) != cudaSuccess ||
+                cudaEventCreateWithFlags(&r.dec_done[i], ef) != cudaSuccess)
+                return nullptr;
+        ready[dev] = true;
+    }
+    return &r;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1083,28 +1155,69 @@ mc_status mc_decode_host(const mc_host_decode_args* h, void* stream) {
     if ((h->h_quantized == nullptr) != (h->d_quantized == nullptr)) return MC_ERR_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const mc_layout& L = *h->layout;
-    if (cudaMemcpyAsync(h->d_blob, h->h_blob, L.total_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    const uint32_t M = L.num_meshlets;
+    const uint64_t ib = (h->flags & MC_DECODE_INDEX_LOCAL_U8X4) ? 4ull : 12ull;   // index bytes per triangle
+    const uint64_t vb = 4ull * L.n_out, qb = 4ull * L.n;                          // bytes per output vertex
+    std::vector<HostChunk> ch;
+    if (h->chunks >= 2 && M >= 2) ch = plan_host_chunks(L, static_cast<const uint8_t*>(h->h_blob), std::min(h->chunks, 64u));
+    if (ch.size() < 2) {   // serial: H2D, decode, D2H on `stream`
+        if (cudaMemcpyAsync(h->d_blob, h->h_blob, L.total_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return MC_ERR_CUDA;
+        mc_decode_args a{h->layout, h->d_blob, 0, M, h->d_indices, h->d_vertices, h->d_quantized, h->flags};
+        mc_status rc = launch(&a, nullptr, s);
+        if (rc != MC_OK) return rc;
+        if (cudaMemcpyAsync(h->h_indices, h->d_indices, ib * L.total_tp, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            return MC_ERR_CUDA;
+        if (h->h_vertices &&
+            cudaMemcpyAsync(h->h_vertices, h->d_vertices, vb * L.total_v, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            return MC_ERR_CUDA;
+        if (h->h_quantized &&
+            cudaMemcpyAsync(h->h_quantized, h->d_quantized, qb * L.total_v, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            return MC_ERR_CUDA;
+        return MC_OK;
+    }
+    // pipelined: copy-in stream -> decode on `stream` -> copy-out stream, one event pair per chunk
+    PipeRes* R = pipe_res();
+    if (!R) return MC_ERR_CUDA;
+    std::lock_guard<std::mutex> g(R->mu);   // the event pool is shared by concurrent callers
+    auto ok = [](cudaError_t e) { return e == cudaSuccess; };
+    const uint8_t* hb = static_cast<const uint8_t*>(h->h_blob);
+    uint8_t* db = static_cast<uint8_t*>(h->d_blob);
+    if (!ok(cudaEventRecord(R->start, s)) || !ok(cudaStreamWaitEvent(R->in, R->start, 0)) ||
+        !ok(cudaStreamWaitEvent(R->out, R->start, 0)))
         return MC_ERR_CUDA;
-    mc_decode_args a;
-    a.layout = h->layout;
-    a.d_blob = h->d_blob;
-    a.first = 0;
-    a.count = L.num_meshlets;
-    a.d_indices = h->d_indices;
-    a.d_vertices = h->d_vertices;
-    a.d_quantized = h->d_quantized;
-    a.flags = h->flags;
-    mc_status rc = launch(&a, nullptr, s);
-    if (rc != MC_OK) return rc;
-    const uint64_t idx_bytes = (h->flags & MC_DECODE_INDEX_LOCAL_U8X4) ? 4ull * L.total_tp : 12ull * L.total_tp;
-    if (cudaMemcpyAsync(h->h_indices, h->d_indices, idx_bytes, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        return MC_ERR_CUDA;
-    if (h->h_vertices &&
-        cudaMemcpyAsync(h->h_vertices, h->d_vertices, 4ull * L.n_out * L.total_v, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        return MC_ERR_CUDA;
-    if (h->h_quantized &&
-        cudaMemcpyAsync(h->h_quantized, h->d_quantized, 4ull * L.n * L.total_v, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        return MC_ERR_CUDA;
+    // header, directory, object and cull tables: everything before the records
+    if (!ok(cudaMemcpyAsync(db, hb, L.off_rec, cudaMemcpyHostToDevice, R->in))) return MC_ERR_CUDA;
+    for (size_t c = 0; c + 1 < ch.size(); ++c) {
+        const HostChunk &a0 = ch[c], &a1 = ch[c + 1];
+        const uint64_t r0 = L.off_rec + a0.rec_off, r1 = L.off_rec + a1.rec_off;
+        if (!ok(cudaMemcpyAsync(db + r0, hb + r0, r1 - r0, cudaMemcpyHostToDevice, R->in)) ||
+            !ok(cudaEventRecord(R->in_done[c], R->in)) || !ok(cudaStreamWaitEvent(s, R->in_done[c], 0)))
+            return MC_ERR_CUDA;
+        mc_decode_args a{h->layout, h->d_blob, a0.first, a1.first - a0.first, h->d_indices, h->d_vertices,
+                         h->d_quantized, h->flags};
+        mc_status rc = launch(&a, nullptr, s);
+        if (rc != MC_OK) return rc;
+        if (!ok(cudaEventRecord(R->dec_done[c], s)) || !ok(cudaStreamWaitEvent(R->out, R->dec_done[c], 0)))
+            return MC_ERR_CUDA;
+        const uint64_t t0 = a0.tri - L.base_tri, t1 = a1.tri - L.base_tri;
+        const uint64_t v0 = a0.vtx - L.base_vtx, v1 = a1.vtx - L.base_vtx;
+        if (t1 > t0 && !ok(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(h->h_indices) + ib * t0,
+                                           reinterpret_cast<const uint8_t*>(h->d_indices) + ib * t0, ib * (t1 - t0),
+                                           cudaMemcpyDeviceToHost, R->out)))
+            return MC_ERR_CUDA;
+        if (h->h_vertices && v1 > v0 &&
+            !ok(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(h->h_vertices) + vb * v0,
+                                reinterpret_cast<const uint8_t*>(h->d_vertices) + vb * v0, vb * (v1 - v0),
+                                cudaMemcpyDeviceToHost, R->out)))
+            return MC_ERR_CUDA;
+        if (h->h_quantized && v1 > v0 &&
+            !ok(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(h->h_quantized) + qb * v0,
+                                reinterpret_cast<const uint8_t*>(h->d_quantized) + qb * v0, qb * (v1 - v0),
+                                cudaMemcpyDeviceToHost, R->out)))
+            return MC_ERR_CUDA;
+    }
+    if (!ok(cudaEventRecord(R->done, R->out)) || !ok(cudaStreamWaitEvent(s, R->done, 0))) return MC_ERR_CUDA;
     return MC_OK;
 }
 

@@ -883,7 +883,7 @@ mc_status parse(const uint8_t* b, size_t nbytes, mc_layout* L) {
 // ================================================================= C ABI (host part)
 extern "C" {
 
-uint32_t mc_abi_version(void) { return 2; }
+uint32_t mc_abi_version(void) { return 3; }
 
 const char* mc_status_str(mc_status s) {
     switch (s) {

@@ -29,7 +29,7 @@ def test_exports_every_declared_symbol(mc):
     L = mc.lib()
     for name in sorted(declared):
         assert hasattr(L, name), name
-    assert L.mc_abi_version() == 2
+    assert L.mc_abi_version() == 3
     out = os.popen(f"nm -D {mc.LIB_PATH}").read()
     for name in declared:
         assert re.search(rf"\bT {name}\b", out), name

@@ -218,21 +218,37 @@ def test_shards_sum_to_whole(mc, orc):
     np.testing.assert_array_equal(np.concatenate(cat), _u32(dbf.indices))
 
 
-def test_decode_host_e2e(mc, orc):
+@pytest.mark.parametrize("chunks", [0, 2, 7, 64])
+@pytest.mark.parametrize("index_format", ["u32", "u8x4"])
+def test_decode_host_e2e(mc, orc, chunks, index_format):
+    """mc_decode_host from pinned host buffers, serial (chunks 0) and pipelined over PCIe
+    (chunks >= 2, more chunks than some records): bit-exact with the oracle; the outputs
+    are poisoned first so a chunk whose copy-out is missing or misplaced shows up."""
     b = mc.mc_encode(synth.torus(100, 50), 64, 126, 2)
     data = np.array(b.bytes)
     L = mc.parse_header(data)
+    u8 = index_format == "u8x4"
+    flags = mc.MC_DECODE_INDEX_LOCAL_U8X4 if u8 else 0
+    nidx = (1 if u8 else 3) * L.total_tp
     h_blob = torch.from_numpy(data).pin_memory()
-    h_idx = torch.empty(3 * L.total_tp, dtype=torch.int32).pin_memory()
-    h_v = torch.empty(L.n_out * L.total_v, dtype=torch.float32).pin_memory()
-    d_blob = torch.empty(data.nbytes, dtype=torch.uint8, device="cuda")
-    d_idx = torch.empty(3 * L.total_tp, dtype=torch.int32, device="cuda")
+    h_idx = torch.full((nidx,), -1, dtype=torch.int32).pin_memory()
+    h_v = torch.full((L.n_out * L.total_v,), -1, dtype=torch.int32).pin_memory().view(torch.float32)
+    h_q = torch.full((L.n * L.total_v,), -1, dtype=torch.int32).pin_memory()
+    d_blob = torch.zeros(data.nbytes, dtype=torch.uint8, device="cuda")
+    d_idx = torch.empty(nidx, dtype=torch.int32, device="cuda")
     d_v = torch.empty(L.n_out * L.total_v, dtype=torch.float32, device="cuda")
-    mc.mc_decode_host(L, h_blob, d_blob, h_idx, d_idx, h_v, d_v)
-    torch.cuda.synchronize()
+    d_q = torch.empty(L.n * L.total_v, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    mc.mc_decode_host(L, h_blob, d_blob, h_idx, d_idx, h_v, d_v, h_q, d_q, flags=flags, stream=s, chunks=chunks)
+    s.synchronize()                      # ordered on the caller's stream, copy streams included
     err, errs, idx, q, f = orc.decode(data)
+    assert err == 0
+    if u8:
+        err8, idx = orc.decode_u8x4(data)
+        assert err8 == 0
     np.testing.assert_array_equal(h_idx.numpy().view(np.uint32), idx)
     np.testing.assert_array_equal(h_v.numpy().view(np.uint32), f.view(np.uint32))
+    np.testing.assert_array_equal(h_q.numpy().view(np.uint32), q)
 
 
 # ------------------------------------------------------------------ malformed streams (FORMAT.md §5)
