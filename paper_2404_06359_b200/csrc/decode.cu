@@ -29,8 +29,10 @@
 // channel, bound by HBM bandwidth.  No --use_fast_math.
 // Compile-time tuning knobs (defaults are the measured optimum on B200, A/B tables in
 // profiles/experiments; scripts/build_variants.sh builds alternatives):
-//   MC_MIN_BLOCKS       __launch_bounds__ min blocks (default: 3 CTAs/SM, 80-register cap
-//                       on every variant except the hot b = 16 octahedral layout)
+//   MC_MIN_BLOCKS       __launch_bounds__ min blocks (default: 3 CTAs/SM = 80-register cap)
+//   MC_WORD_STEP        flag words per topology iteration with 16-lane groups (default 4:
+//                       every N[] of a T~ <= 128 meshlet first, one barrier, then every
+//                       triangle; the per-word broadcasts are shared by its two half-steps)
 //   MC_MAX_CTAS_PER_SM  cap on resident CTAs per SM used to size the persistent grid
 //   MC_GROUP16_TMAX     two meshlets per warp (16-lane groups) when T~ <= this
 //   MC_DYNAMIC          interleaved claim counters (0 = static grid stride)
@@ -59,6 +61,9 @@
 #endif
 #ifndef MC_BANK_PAD
 #define MC_BANK_PAD 1
+#endif
+#ifndef MC_WORD_STEP
+#define MC_WORD_STEP 4   // flag words per step-loop iteration (G = 16; 0 = one G-triangle step at a time)
 #endif
 #ifndef MC_MAX_CTAS_PER_SM
 #define MC_MAX_CTAS_PER_SM 64
@@ -220,10 +225,10 @@ __device__ uint32_t g_position_counters[kCounterBlocks * MC_DYNAMIC];
 // b = 16) so codes are read as aligned halfwords.  NCH == 0: generic
 // runtime layout (any n <= 16, widths 1..24, any octahedral placement).
 // Register budget: 3 CTAs x 8 warps per SM is the measured optimum (profiles/experiments);
-// variants that would otherwise take more than 80 registers are capped to keep 3 CTAs/SM.
+// every variant is capped at 80 registers to keep 3 CTAs/SM.
 template <int NCH, int AM>
 constexpr int min_blocks() {
-    return MC_MIN_BLOCKS > 1 ? MC_MIN_BLOCKS : ((NCH == 7 && AM == 0) ? 1 : 3);
+    return MC_MIN_BLOCKS > 1 ? MC_MIN_BLOCKS : 3;
 }
 
 template <int G, int CODEC, bool STATS, int NCH, int OCT0, int AM>
@@ -394,13 +399,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
         uint32_t* idst = P.idx + (P.u8x4 ? 1ull : 3ull) * (tri_base - P.base_tri);
         uint32_t e2 = 0;
         // a6: store triangle t (FORMAT.md §2): three global u32 indices, or one local u8x4 word
-        auto emit = [&](uint32_t t, uint32_t a0, uint32_t a1, uint32_t a2) {
+        // emit_out takes output values: global u32 indices (vout + local), or local ones
+        // for u8x4; emit adds vout to local indices
+        auto emit_out = [&](uint32_t t, uint32_t o0, uint32_t o1, uint32_t o2) {
             if (P.u8x4) {
-                const uint32_t wd = a0 | (a1 << 8) | (a2 << 16);
+                const uint32_t wd = o0 | (o1 << 8) | (o2 << 16);
                 st_u32(idst + t, wd);
                 if (STATS) ws.cs_idx += mix64((((uint64_t)tri_base + t) << 32) | wd);
             } else {
-                const uint32_t o0 = vout + a0, o1 = vout + a1, o2 = vout + a2;
                 uint32_t* d = idst + 3u * t;
                 st_u32(d, o0);
                 st_u32(d + 1, o1);
@@ -410,7 +416,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
                     ws.cs_idx += mix64((kk << 32) | o0) + mix64(((kk + 1) << 32) | o1) + mix64(((kk + 2) << 32) | o2);
                 }
             }
-            if (STATS) ws.degen += (a0 == a1 || a1 == a2 || a0 == a2) ? 1u : 0u;
+            if (STATS) ws.degen += (o0 == o1 || o1 == o2 || o0 == o2) ? 1u : 0u;
+        };
+        auto emit = [&](uint32_t t, uint32_t a0, uint32_t a1, uint32_t a2) {
+            const uint32_t vo = P.u8x4 ? 0u : vout;
+            emit_out(t, vo + a0, vo + a1, vo + a2);
         };
 
         if constexpr (CODEC == MC_CODEC_BASIC) {
@@ -446,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
         uint32_t incw = 0, pc = 0;
         if (CODEC == MC_CODEC_GTS_REUSE) {
             incw = ((uint32_t)gl < W && !err) ? (R[inc_w + gl] & vm) : 0u;
+            if (gl == 0) incw |= 1u;                 // triangle 0 introduces N[2] (see new_vertex)
             pc = __popc(incw);
         }
 #pragma unroll
@@ -463,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
         const uint32_t pc_excl = gl ? pc_excl_raw : 0u;
         if (CODEC == MC_CODEC_GTS_REUSE) {
             const uint32_t total = __shfl_sync(gm, pc, 7, G);
-            if (!err && total != V - 3u) err |= MC_DERR_COUNTS;
+            if (!err && total != V - 2u) err |= MC_DERR_COUNTS;   // V - 3 flags + the bit-0 sentinel
         }
         if (err) {
             if (STATS && gl == 0) {
@@ -477,51 +488,98 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
 
         // ---------------- a3/a4/a5/a6: topology, one triangle per lane, G per step
         if (gl < 2) Nbuf[gl] = (uint8_t)gl;                                  // N[0], N[1]
-        // branch-free step: every lane computes, only the stores are predicated; N[t+1]
-        // and the pivot come from Nbuf after one group barrier (no neighbour shuffles)
-        const uint32_t nsteps = (Tp + G - 1) / G;
-        for (uint32_t j = 0; j < nsteps; ++j) {
-            const uint32_t t = G * j + gl;
-            const uint32_t wj = (G * j) >> 5;                                // flag word of this step
-            const uint32_t bit = t & 31u;
-            const bool active = t < Tp;
-            const uint32_t lw = __shfl_sync(gm, lrw, wj, G);
-            const int p1 = __shfl_sync(gm, prev1, wj, G), p0 = __shfl_sync(gm, prev0, wj, G);
-            // a3: new-vertex index N[t+2] (w_0 := N[2] = 2); the byte read is always inside
-            // the group's shared memory (index masked to 8 bits), used only where valid
+        // a3: new-vertex index N[t+2] of triangle t (local), every lane computes; the byte
+        // read is always inside the group's shared memory (index masked to 8 bits)
+        auto new_vertex = [&](uint32_t t, uint32_t bit, uint32_t iw, uint32_t pcx) -> uint32_t {
             uint32_t w;
             if (CODEC == MC_CODEC_GTS) {
                 const uint32_t bv = BY[(t - 1u) & 0xFFu];
-                w = t ? bv : 2u;
-                if (STATS && active && w >= V) e2 |= MC_DERR_INDEX;
+                w = t ? bv : 2u;                                             // w_0 := N[2] = 2
+                if (STATS && t < Tp && w >= V) e2 |= MC_DERR_INDEX;
             } else {
-                const uint32_t iw = __shfl_sync(gm, incw, wj, G);
-                const uint32_t c = __shfl_sync(gm, pc_excl, wj, G) + __popc(iw & (0xFFFFFFFFu >> (31u - bit)));   // inclusive c_t
-                const uint32_t rv = BY[(t - c - 1u) & 0xFFu];                // location t+1-s, s = 2+c
+                // bit 0 of word 0 is set in incw (triangle 0 "introduces" N[2] = 2), so the
+                // inclusive count is c' = c_t + 1 and N[t+2] = i_t ? 1 + c' : reuse[t - c']
+                const uint32_t c1 = pcx + __popc(iw & (0xFFFFFFFFu >> (31u - bit)));
+                const uint32_t rv = BY[(t - c1) & 0xFFu];                    // location t+1-s, s = 2+c
                 const bool inc = (iw >> bit) & 1u;
-                w = inc ? 2u + c : (t ? rv : 2u);
-                if (STATS && active && !inc && t && w >= V) e2 |= MC_DERR_REUSE;
+                w = inc ? 1u + c1 : rv;
+                if (STATS && t < Tp && !inc && w >= V) e2 |= MC_DERR_REUSE;
             }
-            if (active) Nbuf[t + 2u] = (uint8_t)w;
-            __syncwarp(gm);
+            return w;
+        };
+        // a4/a5/a6 for triangle t once N[0..t+2] is in Nbuf; wg = N[t+2]
+        auto assemble = [&](uint32_t t, uint32_t bit, uint32_t wj, uint32_t lw, int p0, int p1, uint32_t wg) {
             // a4: j(t) = max{k < t : f_k != f_t} by bit scan; earlier words
-            // through the per-word last-R / last-L scans instead of a loop
-            const uint32_t nprev = Nbuf[t + 1u];                             // N[t+1]
+            // through the per-word last-R / last-L scans instead of a loop.  Triangle 0
+            // needs no special case: f_0 = L, x = 0, j = -1, so (N[0], N[1], N[2]).
+            const uint32_t nprev = Nbuf[t + 1u];                            // N[t+1]
             const uint32_t f = (lw >> bit) & 1u;
             const uint32_t x = (f ? ~lw : lw) & ((1u << bit) - 1u);
             const int hi = (int)(32u * wj) + 31 - __clz(x);                  // computed even for x = 0
             const int pw = f ? p0 : p1;
             const int jj = x ? hi : pw;                                      // select, no branch
-            const uint32_t npiv = Nbuf[jj + 1];                              // N[j+1], N[0] if none
-            uint32_t a0 = f ? nprev : npiv, a1 = f ? npiv : nprev;           // a5 (FORMAT.md §2)
-            a0 = t ? a0 : 0u;
-            a1 = t ? a1 : 1u;
-            if (active) {
-                emit(t, a0, a1, w);                                          // a6
+            const uint32_t npiv = Nbuf[jj + 1];                             // N[j+1], N[0] if none
+            const uint32_t a0 = f ? nprev : npiv, a1 = f ? npiv : nprev;     // a5 (FORMAT.md §2)
+            if (t < Tp) {
+                emit(t, a0, a1, wg);                                         // a6
                 if (STATS) {
                     if (t > 0) ws.max_lb = max(ws.max_lb, (uint32_t)((int)t - jj));
                     if (t > 0 && !x && wj > 0) ws.multi++;
                 }
+            }
+        };
+        // branch-free steps: every lane computes, only the stores are predicated; N[t+1]
+        // and the pivot come from Nbuf after one group barrier (no neighbour shuffles)
+        if (MC_WORD_STEP && G == 16) {
+            // MC_WORD_STEP flag words per iteration: each word's two half-steps (triangles
+            // t0 = 32 wj + gl and t1 = t0 + 16) share the word broadcasts, and all of the
+            // iteration's N[] stores share one barrier (independent work for the scheduler)
+            constexpr uint32_t K = MC_WORD_STEP > 0 ? MC_WORD_STEP : 1;
+            for (uint32_t wb = 0; wb < W; wb += K) {
+                uint32_t lw[K], wv0[K], wv1[K];
+                int p1[K], p0[K];
+#pragma unroll
+                for (uint32_t k = 0; k < K; ++k) {
+                    const uint32_t wj = wb + k;      // may pass W: then every t >= T' (no stores)
+                    lw[k] = __shfl_sync(gm, lrw, wj & 7u, G);
+                    p1[k] = __shfl_sync(gm, prev1, wj & 7u, G);
+                    p0[k] = __shfl_sync(gm, prev0, wj & 7u, G);
+                    uint32_t iw = 0, pcx = 0;
+                    if (CODEC == MC_CODEC_GTS_REUSE) {
+                        iw = __shfl_sync(gm, incw, wj & 7u, G);
+                        pcx = __shfl_sync(gm, pc_excl, wj & 7u, G);
+                    }
+                    const uint32_t t0 = 32u * wj + gl, t1 = t0 + 16u;
+                    wv0[k] = new_vertex(t0, gl, iw, pcx);
+                    wv1[k] = new_vertex(t1, gl + 16u, iw, pcx);
+                    if (t0 < Tp) Nbuf[t0 + 2u] = (uint8_t)wv0[k];
+                    if (t1 < Tp) Nbuf[t1 + 2u] = (uint8_t)wv1[k];
+                }
+                __syncwarp(gm);
+#pragma unroll
+                for (uint32_t k = 0; k < K; ++k) {
+                    const uint32_t wj = wb + k, t0 = 32u * wj + gl;
+                    assemble(t0, gl, wj, lw[k], p0[k], p1[k], wv0[k]);
+                    assemble(t0 + 16u, gl + 16u, wj, lw[k], p0[k], p1[k], wv1[k]);
+                }
+            }
+        } else {
+            const uint32_t nsteps = (Tp + G - 1) / G;
+            for (uint32_t j = 0; j < nsteps; ++j) {
+                const uint32_t t = G * j + gl;
+                const uint32_t wj = (G * j) >> 5;                            // flag word of this step
+                const uint32_t bit = t & 31u;
+                const uint32_t lw = __shfl_sync(gm, lrw, wj, G);
+                const int p1 = __shfl_sync(gm, prev1, wj, G), p0 = __shfl_sync(gm, prev0, wj, G);
+                uint32_t iw = 0, pcx = 0;
+                if (CODEC == MC_CODEC_GTS_REUSE) {
+                    iw = __shfl_sync(gm, incw, wj, G);
+                    pcx = __shfl_sync(gm, pc_excl, wj, G);
+                }
+                const uint32_t w = new_vertex(t, bit, iw, pcx);
+                if (t < Tp) Nbuf[t + 2u] = (uint8_t)w;
+                __syncwarp(gm);
+                assemble(t, bit, wj, lw, p0, p1, w);
             }
         }
         }   // strip codecs
