@@ -33,6 +33,7 @@
 //   MC_WORD_STEP        flag words per topology iteration with 16-lane groups (default 4:
 //                       every N[] of a T~ <= 128 meshlet first, one barrier, then every
 //                       triangle; the per-word broadcasts are shared by its two half-steps)
+//   MC_WORD_STEP32      the same for 32-lane groups (T~ > 128)
 //   MC_MAX_CTAS_PER_SM  cap on resident CTAs per SM used to size the persistent grid
 //   MC_GROUP16_TMAX     two meshlets per warp (16-lane groups) when T~ <= this
 //   MC_DYNAMIC          interleaved claim counters (0 = static grid stride)
@@ -63,7 +64,10 @@
 #define MC_BANK_PAD 1
 #endif
 #ifndef MC_WORD_STEP
-#define MC_WORD_STEP 4   // flag words per step-loop iteration (G = 16; 0 = one G-triangle step at a time)
+#define MC_WORD_STEP 4   // flag words per topology iteration, 16-lane groups
+#endif
+#ifndef MC_WORD_STEP32
+#define MC_WORD_STEP32 8 // flag words per topology iteration, 32-lane groups (T~ > 128)
 #endif
 #ifndef MC_MAX_CTAS_PER_SM
 #define MC_MAX_CTAS_PER_SM 64
@@ -530,56 +534,43 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
         };
         // branch-free steps: every lane computes, only the stores are predicated; N[t+1]
         // and the pivot come from Nbuf after one group barrier (no neighbour shuffles)
-        if (MC_WORD_STEP && G == 16) {
-            // MC_WORD_STEP flag words per iteration: each word's two half-steps (triangles
-            // t0 = 32 wj + gl and t1 = t0 + 16) share the word broadcasts, and all of the
+        {
+            // K flag words per iteration; each word is HS = 32/G steps of G triangles
+            // (t = 32 wj + G h + gl) that share the word's broadcasts, and all of the
             // iteration's N[] stores share one barrier (independent work for the scheduler)
-            constexpr uint32_t K = MC_WORD_STEP > 0 ? MC_WORD_STEP : 1;
+            constexpr uint32_t HS = 32 / G;
+            constexpr uint32_t K = G == 16 ? MC_WORD_STEP : MC_WORD_STEP32;
+            static_assert(K == 1 || K == 2 || K == 4 || K == 8, "words per iteration must divide 8");
             for (uint32_t wb = 0; wb < W; wb += K) {
-                uint32_t lw[K], wv0[K], wv1[K];
+                uint32_t lw[K], wv[K][HS];
                 int p1[K], p0[K];
 #pragma unroll
                 for (uint32_t k = 0; k < K; ++k) {
                     const uint32_t wj = wb + k;      // may pass W: then every t >= T' (no stores)
-                    lw[k] = __shfl_sync(gm, lrw, wj & 7u, G);
-                    p1[k] = __shfl_sync(gm, prev1, wj & 7u, G);
-                    p0[k] = __shfl_sync(gm, prev0, wj & 7u, G);
+                    lw[k] = __shfl_sync(gm, lrw, wj, G);
+                    p1[k] = __shfl_sync(gm, prev1, wj, G);
+                    p0[k] = __shfl_sync(gm, prev0, wj, G);
                     uint32_t iw = 0, pcx = 0;
                     if (CODEC == MC_CODEC_GTS_REUSE) {
-                        iw = __shfl_sync(gm, incw, wj & 7u, G);
-                        pcx = __shfl_sync(gm, pc_excl, wj & 7u, G);
+                        iw = __shfl_sync(gm, incw, wj, G);
+                        pcx = __shfl_sync(gm, pc_excl, wj, G);
                     }
-                    const uint32_t t0 = 32u * wj + gl, t1 = t0 + 16u;
-                    wv0[k] = new_vertex(t0, gl, iw, pcx);
-                    wv1[k] = new_vertex(t1, gl + 16u, iw, pcx);
-                    if (t0 < Tp) Nbuf[t0 + 2u] = (uint8_t)wv0[k];
-                    if (t1 < Tp) Nbuf[t1 + 2u] = (uint8_t)wv1[k];
+#pragma unroll
+                    for (uint32_t h = 0; h < HS; ++h) {
+                        const uint32_t bit = G * h + gl, t = 32u * wj + bit;
+                        wv[k][h] = new_vertex(t, bit, iw, pcx);
+                        if (t < Tp) Nbuf[t + 2u] = (uint8_t)wv[k][h];
+                    }
                 }
                 __syncwarp(gm);
 #pragma unroll
                 for (uint32_t k = 0; k < K; ++k) {
-                    const uint32_t wj = wb + k, t0 = 32u * wj + gl;
-                    assemble(t0, gl, wj, lw[k], p0[k], p1[k], wv0[k]);
-                    assemble(t0 + 16u, gl + 16u, wj, lw[k], p0[k], p1[k], wv1[k]);
+#pragma unroll
+                    for (uint32_t h = 0; h < HS; ++h) {
+                        const uint32_t wj = wb + k, bit = G * h + gl;
+                        assemble(32u * wj + bit, bit, wj, lw[k], p0[k], p1[k], wv[k][h]);
+                    }
                 }
-            }
-        } else {
-            const uint32_t nsteps = (Tp + G - 1) / G;
-            for (uint32_t j = 0; j < nsteps; ++j) {
-                const uint32_t t = G * j + gl;
-                const uint32_t wj = (G * j) >> 5;                            // flag word of this step
-                const uint32_t bit = t & 31u;
-                const uint32_t lw = __shfl_sync(gm, lrw, wj, G);
-                const int p1 = __shfl_sync(gm, prev1, wj, G), p0 = __shfl_sync(gm, prev0, wj, G);
-                uint32_t iw = 0, pcx = 0;
-                if (CODEC == MC_CODEC_GTS_REUSE) {
-                    iw = __shfl_sync(gm, incw, wj, G);
-                    pcx = __shfl_sync(gm, pc_excl, wj, G);
-                }
-                const uint32_t w = new_vertex(t, bit, iw, pcx);
-                if (t < Tp) Nbuf[t + 2u] = (uint8_t)w;
-                __syncwarp(gm);
-                assemble(t, bit, wj, lw, p0, p1, w);
             }
         }
         }   // strip codecs

@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--k", type=int, default=300)
     ap.add_argument("--codec", type=int, default=2)
     ap.add_argument("--label", default="")
+    ap.add_argument("--sizes", default="", help="subset, e.g. 128x256,256x256")
+    ap.add_argument("--bits", default="", help="subset, e.g. 16,24")
     args = ap.parse_args()
     import torch
     import paper_2404_06359_b200 as mc
@@ -50,8 +52,10 @@ def main():
     mesh = synth.displaced_sphere(args.k, oct_normals=False)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     out = open(args.out, "a")
-    for (vm, tm) in SIZES:
-        for b in BITS:
+    sizes = [tuple(int(x) for x in p.split("x")) for p in args.sizes.split(",")] if args.sizes else SIZES
+    bits = [int(x) for x in args.bits.split(",")] if args.bits else BITS
+    for (vm, tm) in sizes:
+        for b in bits:
             t0 = time.time()
             proto = mc.mc_encode(mesh.with_bits(b), vm, tm, args.codec)
             n = args.instances
