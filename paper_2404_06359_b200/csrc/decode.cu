@@ -235,7 +235,7 @@ constexpr int min_blocks() {
     return MC_MIN_BLOCKS > 1 ? MC_MIN_BLOCKS : 3;
 }
 
-template <int G, int CODEC, bool STATS, int NCH, int OCT0, int AM>
+template <int G, int KW, int CODEC, bool STATS, int NCH, int OCT0, int AM>
 __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_kernel(const __grid_constant__ Params P) {
     static_assert(G == 8 || G == 16 || G == 32, "group size");
     constexpr bool B16 = AM == 0, VWK = AM == 2;
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
             // (t = 32 wj + G h + gl) that share the word's broadcasts, and all of the
             // iteration's N[] stores share one barrier (independent work for the scheduler)
             constexpr uint32_t HS = 32 / G;
-            constexpr uint32_t K = G == 16 ? MC_WORD_STEP : MC_WORD_STEP32;
+            constexpr uint32_t K = KW;
             static_assert(K == 1 || K == 2 || K == 4 || K == 8, "words per iteration must divide 8");
             for (uint32_t wb = 0; wb < W; wb += K) {
                 uint32_t lw[K], wv[K][HS];
@@ -936,9 +936,9 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     return MC_OK;
 }
 
-template <int G, int CODEC, bool STATS, int NCH, int OCT0, int AM>
+template <int G, int KW, int CODEC, bool STATS, int NCH, int OCT0, int AM>
 mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
-    auto kern = mc_decode_kernel<G, CODEC, STATS, NCH, OCT0, AM>;
+    auto kern = mc_decode_kernel<G, KW, CODEC, STATS, NCH, OCT0, AM>;
     constexpr uint32_t NG = 32 / G;
     const size_t warp_smem = NG * grp_smem;
     // warps per CTA: 8, fewer when a warp's staging buffers are large (Ṽ=T̃=256, 24-bit)
@@ -994,8 +994,11 @@ mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
 // MC_GROUP16_TMAX decoded triangles, else one meshlet per warp (G = 32)
 template <int CODEC, bool STATS, int NCH, int OCT0, int AM>
 mc_status launch_t(const Params& P, size_t grp_smem, cudaStream_t s) {
-    if (P.tmax <= MC_GROUP16_TMAX) return launch_g<16, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
-    return launch_g<32, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
+    // flag words per topology iteration: every word of a T~-triangle meshlet at once
+    // (MC_WORD_STEP / MC_WORD_STEP32), one word when T~ <= 32 (no empty words)
+    if (P.tmax <= 32) return launch_g<16, 1, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
+    if (P.tmax <= MC_GROUP16_TMAX) return launch_g<16, MC_WORD_STEP, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
+    return launch_g<32, MC_WORD_STEP32, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
 }
 
 template <int CODEC, bool STATS, int NCH, int OCT0>
