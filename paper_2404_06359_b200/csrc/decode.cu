@@ -37,6 +37,7 @@
 //   MC_MAX_CTAS_PER_SM  cap on resident CTAs per SM used to size the persistent grid
 //   MC_GROUP16_TMAX     two meshlets per warp (16-lane groups) when T~ <= this
 //   MC_DYNAMIC          interleaved claim counters (0 = static grid stride)
+//   MC_STATIC_BELOW     launches with fewer records per group use the static stride
 //   MC_ST_CS            streaming (.cs) output stores
 //   MC_BANK_PAD         group smem stride = 16 (mod 32) words
 #include "../../include/mc.h"
@@ -56,6 +57,9 @@
 #endif
 #ifndef MC_GROUP16_TMAX
 #define MC_GROUP16_TMAX 128
+#endif
+#ifndef MC_STATIC_BELOW
+#define MC_STATIC_BELOW 8   // records per group below which a launch uses the static grid stride
 #endif
 #ifndef MC_DYNAMIC
 #define MC_DYNAMIC 128   // interleaved claim streams (0 = static grid stride)
@@ -275,9 +279,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
     // MC_DYNAMIC interleaved streams: positions s, s + NS, s + 2 NS, ... are handed out by
     // counter s (= group id mod NS), so claims stay in global order (neighbouring records
     // decoded at about the same time) while each counter sees 1/NS of the atomics
+    // (launches of fewer than MC_STATIC_BELOW records per group pass ctr = null and use the
+    // static grid stride: no counter memset, no atomics on the latency-bound short path)
     constexpr uint32_t NS = MC_DYNAMIC;
     const uint32_t stream = gg % NS;
-    auto grab = [&]() -> uint32_t { return base0 + stream + NS * atomicAdd(P.ctr + stream, 1u); };
+    const uint32_t ngroups = gridDim.x * wpc * NG;
+    uint32_t grabbed = 0;
+    auto grab = [&]() -> uint32_t {
+        return P.ctr ? base0 + stream + NS * atomicAdd(P.ctr + stream, 1u) : base0 + gg + (grabbed++) * ngroups;
+    };
 #else
     const uint32_t ngroups = gridDim.x * wpc * NG;
     uint32_t grabbed = 0;
@@ -971,8 +981,13 @@ mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
         bps_cache[wpc][bucket] = bps;
     }
     Params PL = P;
+    const uint32_t count = P.end - P.first;
+    const uint64_t want = (count + wpc * NG - 1) / (wpc * NG);
+    const uint64_t cap = (uint64_t)sms * std::min(bps, MC_MAX_CTAS_PER_SM);
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
+    PL.ctr = nullptr;
 #if MC_DYNAMIC
-    {
+    if (P.list || (uint64_t)count >= (uint64_t)MC_STATIC_BELOW * grid * wpc * NG) {
         static uint32_t* slots = nullptr;
         static uint32_t seq = 0;
         std::lock_guard<std::mutex> g(mu);
@@ -982,10 +997,6 @@ mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
         if (cudaMemsetAsync(PL.ctr, 0, 4 * MC_DYNAMIC, s) != cudaSuccess) return MC_ERR_CUDA;
     }
 #endif
-    const uint32_t count = P.end - P.first;
-    const uint64_t want = (count + wpc * NG - 1) / (wpc * NG);
-    const uint64_t cap = (uint64_t)sms * std::min(bps, MC_MAX_CTAS_PER_SM);
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
     kern<<<grid, 32 * wpc, smem, s>>>(PL);
     return cudaGetLastError() == cudaSuccess ? MC_OK : MC_ERR_CUDA;
 }
