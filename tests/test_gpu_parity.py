@@ -169,6 +169,46 @@ def test_max_sizes(mc, orc):
     gpu_vs_oracle(mc, orc, blob)
 
 
+@pytest.mark.parametrize("n,sem", [(7, [1, 1, 1, 4, 4, 3, 3]), (8, [1, 1, 1, 2, 2, 2, 3, 3]), (3, [1, 1, 1])])
+@pytest.mark.parametrize("b", [16, 12])
+def test_int_to_float_boundary(mc, orc, n, sem, b):
+    """Grid values q = L_c + code on both sides of 2^23: records whose every q < 2^23 take the
+    exact bit-trick conversion (0x4B000000 + q as a float, minus 2^23), the others the
+    conversion instruction; both must give the oracle's (float)q bit for bit (FORMAT.md §4)."""
+    rng = np.random.default_rng(11 + n + b)
+    bm = (1 << b) - 1
+    M = 240
+    ms, codes, L = [], [], []
+    edge = (1 << 23) - 1 - bm
+    for k in range(M):
+        Tp = int(rng.integers(1, 127))
+        V = int(rng.integers(3, 65))
+        ms.append(gts_meshlet(V, rng.integers(0, 2, size=Tp - 1), rng.integers(0, V, size=Tp - 1)))
+        c = rng.integers(0, bm + 1, size=V * n)
+        if k % 4 == 0:
+            c[rng.integers(0, V * n)] = bm                        # largest code present
+        codes.append(c)
+        mode = k % 6
+        if mode == 0:
+            Lk = np.full(n, edge)                                 # q reaches 2^23 - 1: fast path
+        elif mode == 1:
+            Lk = np.full(n, edge); Lk[rng.integers(0, n)] += 1    # one channel may reach 2^23
+        elif mode == 2:
+            Lk = rng.integers(0, edge + 1, size=n)
+        elif mode == 3:
+            Lk = rng.integers(edge - 5, edge + 6, size=n)
+        elif mode == 4:
+            Lk = rng.integers(1 << 23, 1 << 28, size=n)           # large q: conversion instruction
+        else:
+            Lk = rng.integers(0, 1 << 12, size=n)
+        L.append(Lk)
+    delta = np.full(n, 1e-7, np.float32)
+    origin = np.full(n, -0.5, np.float32)
+    blob = pack_meshlets(orc, 1, ms, n=n, bits=[b] * n, sem=sem, codes=np.concatenate(codes),
+                         L=np.concatenate(L).astype(np.uint32), delta=delta, origin=origin, vmax=64, tmax=126)
+    gpu_vs_oracle(mc, orc, blob)
+
+
 def test_empty_and_ragged(mc, orc):
     e = orc.encode(synth.quad_grid(2, 1), 64, 126, 2)
     gpu_vs_oracle(mc, orc, e.blob)
