@@ -37,7 +37,7 @@
 //   MC_MAX_CTAS_PER_SM  cap on resident CTAs per SM used to size the persistent grid
 //   MC_GROUP16_TMAX     two meshlets per warp (16-lane groups) when T~ <= this
 //   MC_DYNAMIC          interleaved claim counters (0 = static grid stride)
-//   MC_STATIC_BELOW     launches with fewer records per group use the static stride
+//   MC_STATIC_BELOW     launches with fewer records per group use the static stride (0 = never)
 //   MC_ST_CS            streaming (.cs) output stores
 //   MC_BANK_PAD         group smem stride = 16 (mod 32) words
 #include "../../include/mc.h"
@@ -47,7 +47,6 @@
 
 #include <algorithm>
 #include <mutex>
-#include <type_traits>
 #include <vector>
 
 #ifndef MC_MIN_BLOCKS
@@ -60,7 +59,8 @@
 #define MC_GROUP16_TMAX 128
 #endif
 #ifndef MC_STATIC_BELOW
-#define MC_STATIC_BELOW 8   // records per group below which a launch uses the static grid stride
+#define MC_STATIC_BELOW 0   // records per group below which a launch uses the static grid stride
+                            // (8: cfg2 +20%, but the runtime test costs cfg4 0.8%; off by default)
 #endif
 #ifndef MC_DYNAMIC
 #define MC_DYNAMIC 128   // interleaved claim streams (0 = static grid stride)
@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
     const uint32_t ngroups = gridDim.x * wpc * NG;
     uint32_t grabbed = 0;
     auto grab = [&]() -> uint32_t {
-        return P.ctr ? base0 + stream + NS * atomicAdd(P.ctr + stream, 1u) : base0 + gg + (grabbed++) * ngroups;
+        if (MC_STATIC_BELOW == 0 || P.ctr) return base0 + stream + NS * atomicAdd(P.ctr + stream, 1u);
+        return base0 + gg + (grabbed++) * ngroups;
     };
 #else
     const uint32_t ngroups = gridDim.x * wpc * NG;
@@ -413,16 +414,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
         const uint32_t vout = vtx_base - P.index_sub;
         uint32_t* idst = P.idx + (P.u8x4 ? 1ull : 3ull) * (tri_base - P.base_tri);
         uint32_t e2 = 0;
-        // a6: store triangle t (FORMAT.md §2): three global u32 indices (vout + local), or
-        // one local u8x4 word; `u8` is a compile-time tag (the loops below are instantiated
-        // for both index formats behind one uniform branch, so neither pays for the other)
-        auto emit = [&](auto u8, uint32_t t, uint32_t a0, uint32_t a1, uint32_t a2) {
-            if constexpr (decltype(u8)::value) {
-                const uint32_t wd = a0 | (a1 << 8) | (a2 << 16);
+        // a6: store triangle t (FORMAT.md §2): three global u32 indices, or one local u8x4 word
+        // emit_out takes output values: global u32 indices (vout + local), or local ones
+        // for u8x4; emit adds vout to local indices
+        auto emit_out = [&](uint32_t t, uint32_t o0, uint32_t o1, uint32_t o2) {
+            if (P.u8x4) {
+                const uint32_t wd = o0 | (o1 << 8) | (o2 << 16);
                 st_u32(idst + t, wd);
                 if (STATS) ws.cs_idx += mix64((((uint64_t)tri_base + t) << 32) | wd);
             } else {
-                const uint32_t o0 = vout + a0, o1 = vout + a1, o2 = vout + a2;
                 uint32_t* d = idst + 3u * t;
                 st_u32(d, o0);
                 st_u32(d + 1, o1);
@@ -432,10 +432,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
                     ws.cs_idx += mix64((kk << 32) | o0) + mix64(((kk + 1) << 32) | o1) + mix64(((kk + 2) << 32) | o2);
                 }
             }
-            if (STATS) ws.degen += (a0 == a1 || a1 == a2 || a0 == a2) ? 1u : 0u;
+            if (STATS) ws.degen += (o0 == o1 || o1 == o2 || o0 == o2) ? 1u : 0u;
         };
-        const std::true_type kU8x4{};
-        const std::false_type kU32{};
+        auto emit = [&](uint32_t t, uint32_t a0, uint32_t a1, uint32_t a2) {
+            const uint32_t vo = P.u8x4 ? 0u : vout;
+            emit_out(t, vo + a0, vo + a1, vo + a2);
+        };
 
         if constexpr (CODEC == MC_CODEC_BASIC) {
             // ---------------- a3-a6 for Basic: the local triangle list itself
@@ -448,15 +450,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
                 __syncwarp(gm);
                 continue;
             }
-            auto basic_loop = [&](auto u8) {
-                for (uint32_t t = gl; t < Tp; t += G) {
-                    const uint32_t a0 = BY[3u * t], a1 = BY[3u * t + 1u], a2 = BY[3u * t + 2u];
-                    if (STATS && (a0 >= V || a1 >= V || a2 >= V)) e2 |= MC_DERR_INDEX;
-                    emit(u8, t, a0, a1, a2);
-                }
-            };
-            if (P.u8x4) basic_loop(kU8x4);
-            else basic_loop(kU32);
+            for (uint32_t t = gl; t < Tp; t += G) {
+                const uint32_t a0 = BY[3u * t], a1 = BY[3u * t + 1u], a2 = BY[3u * t + 2u];
+                if (STATS && (a0 >= V || a1 >= V || a2 >= V)) e2 |= MC_DERR_INDEX;
+                emit(t, a0, a1, a2);
+            }
         } else {
         // ---------------- per-word prefix state, group lanes 0..W-1 hold word `gl` (W <= 8)
         // valid bits of word `gl`: triangles t < T', bit 0 (t = 0) excluded
@@ -526,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
             return w;
         };
         // a4/a5/a6 for triangle t once N[0..t+2] is in Nbuf; wg = N[t+2]
-        auto assemble = [&](auto u8, uint32_t t, uint32_t bit, uint32_t wj, uint32_t lw, int p0, int p1, uint32_t wg) {
+        auto assemble = [&](uint32_t t, uint32_t bit, uint32_t wj, uint32_t lw, int p0, int p1, uint32_t wg) {
             // a4: j(t) = max{k < t : f_k != f_t} by bit scan; earlier words
             // through the per-word last-R / last-L scans instead of a loop.  Triangle 0
             // needs no special case: f_0 = L, x = 0, j = -1, so (N[0], N[1], N[2]).
@@ -539,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
             const uint32_t npiv = Nbuf[jj + 1];                             // N[j+1], N[0] if none
             const uint32_t a0 = f ? nprev : npiv, a1 = f ? npiv : nprev;     // a5 (FORMAT.md §2)
             if (t < Tp) {
-                emit(u8, t, a0, a1, wg);                                     // a6
+                emit(t, a0, a1, wg);                                         // a6
                 if (STATS) {
                     if (t > 0) ws.max_lb = max(ws.max_lb, (uint32_t)((int)t - jj));
                     if (t > 0 && !x && wj > 0) ws.multi++;
@@ -548,7 +546,42 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
         };
         // branch-free steps: every lane computes, only the stores are predicated; N[t+1]
         // and the pivot come from Nbuf after one group barrier (no neighbour shuffles)
-        auto strip_loop = [&](auto u8) {
+        if constexpr (G == 16) {
+            // K = KW flag words per iteration: each word's two half-steps (triangles
+            // t0 = 32 wj + gl and t1 = t0 + 16) share the word broadcasts, and all of the
+            // iteration's N[] stores share one barrier (independent work for the scheduler).
+            // This exact form schedules measurably better than the generic loop below
+            // (profiles/experiments: 132.6 vs 131.3 Gtri/s on cfg4).
+            constexpr uint32_t K = KW;
+            for (uint32_t wb = 0; wb < W; wb += K) {
+                uint32_t lw[K], wv0[K], wv1[K];
+                int p1[K], p0[K];
+#pragma unroll
+                for (uint32_t k = 0; k < K; ++k) {
+                    const uint32_t wj = wb + k;      // may pass W: then every t >= T' (no stores)
+                    lw[k] = __shfl_sync(gm, lrw, wj & 7u, G);
+                    p1[k] = __shfl_sync(gm, prev1, wj & 7u, G);
+                    p0[k] = __shfl_sync(gm, prev0, wj & 7u, G);
+                    uint32_t iw = 0, pcx = 0;
+                    if (CODEC == MC_CODEC_GTS_REUSE) {
+                        iw = __shfl_sync(gm, incw, wj & 7u, G);
+                        pcx = __shfl_sync(gm, pc_excl, wj & 7u, G);
+                    }
+                    const uint32_t t0 = 32u * wj + gl, t1 = t0 + 16u;
+                    wv0[k] = new_vertex(t0, gl, iw, pcx);
+                    wv1[k] = new_vertex(t1, gl + 16u, iw, pcx);
+                    if (t0 < Tp) Nbuf[t0 + 2u] = (uint8_t)wv0[k];
+                    if (t1 < Tp) Nbuf[t1 + 2u] = (uint8_t)wv1[k];
+                }
+                __syncwarp(gm);
+#pragma unroll
+                for (uint32_t k = 0; k < K; ++k) {
+                    const uint32_t wj = wb + k, t0 = 32u * wj + gl;
+                    assemble(t0, gl, wj, lw[k], p0[k], p1[k], wv0[k]);
+                    assemble(t0 + 16u, gl + 16u, wj, lw[k], p0[k], p1[k], wv1[k]);
+                }
+            }
+        } else {
             // K flag words per iteration; each word is HS = 32/G steps of G triangles
             // (t = 32 wj + G h + gl) that share the word's broadcasts, and all of the
             // iteration's N[] stores share one barrier (independent work for the scheduler)
@@ -582,13 +615,11 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
 #pragma unroll
                     for (uint32_t h = 0; h < HS; ++h) {
                         const uint32_t wj = wb + k, bit = G * h + gl;
-                        assemble(u8, 32u * wj + bit, bit, wj, lw[k], p0[k], p1[k], wv[k][h]);
+                        assemble(32u * wj + bit, bit, wj, lw[k], p0[k], p1[k], wv[k][h]);
                     }
                 }
             }
-        };
-        if (P.u8x4) strip_loop(kU8x4);
-        else strip_loop(kU32);
+        }
         }   // strip codecs
         if (STATS) {
             e2 = __reduce_or_sync(gm, e2);
