@@ -68,6 +68,9 @@
 #ifndef MC_BANK_PAD
 #define MC_BANK_PAD 1
 #endif
+#ifndef MC_U8_KERNEL
+#define MC_U8_KERNEL 1   // separate u8x4-only kernels for the compile-time halfword layouts
+#endif
 #ifndef MC_WORD_STEP
 #define MC_WORD_STEP 4   // flag words per topology iteration, 16-lane groups
 #endif
@@ -240,7 +243,7 @@ constexpr int min_blocks() {
     return MC_MIN_BLOCKS > 1 ? MC_MIN_BLOCKS : 3;
 }
 
-template <int G, int KW, int CODEC, bool STATS, int NCH, int OCT0, int AM>
+template <int G, int KW, int CODEC, bool STATS, int NCH, int OCT0, int AM, bool U8 = false>
 __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_kernel(const __grid_constant__ Params P) {
     static_assert(G == 8 || G == 16 || G == 32, "group size");
     constexpr bool B16 = AM == 0, VWK = AM == 2;
@@ -412,13 +415,17 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
         const uint8_t* BY = reinterpret_cast<const uint8_t*>(R + by_w);
         const uint32_t* AT = R + at_w;
         const uint32_t vout = vtx_base - P.index_sub;
-        uint32_t* idst = P.idx + (P.u8x4 ? 1ull : 3ull) * (tri_base - P.base_tri);
+        // U8: a kernel built for the u8x4 index format only (no u32 emit path at all); the
+        // default kernel reads the format flag at run time (its if-converted form is the
+        // fastest u32 kernel, profiles/experiments)
+        const bool u8x4 = U8 || P.u8x4;
+        uint32_t* idst = P.idx + (u8x4 ? 1ull : 3ull) * (tri_base - P.base_tri);
         uint32_t e2 = 0;
         // a6: store triangle t (FORMAT.md §2): three global u32 indices, or one local u8x4 word
         // emit_out takes output values: global u32 indices (vout + local), or local ones
         // for u8x4; emit adds vout to local indices
         auto emit_out = [&](uint32_t t, uint32_t o0, uint32_t o1, uint32_t o2) {
-            if (P.u8x4) {
+            if (u8x4) {
                 const uint32_t wd = o0 | (o1 << 8) | (o2 << 16);
                 st_u32(idst + t, wd);
                 if (STATS) ws.cs_idx += mix64((((uint64_t)tri_base + t) << 32) | wd);
@@ -435,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
             if (STATS) ws.degen += (o0 == o1 || o1 == o2 || o0 == o2) ? 1u : 0u;
         };
         auto emit = [&](uint32_t t, uint32_t a0, uint32_t a1, uint32_t a2) {
-            const uint32_t vo = P.u8x4 ? 0u : vout;
+            const uint32_t vo = u8x4 ? 0u : vout;
             emit_out(t, vo + a0, vo + a1, vo + a2);
         };
 
@@ -983,9 +990,9 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     return MC_OK;
 }
 
-template <int G, int KW, int CODEC, bool STATS, int NCH, int OCT0, int AM>
+template <int G, int KW, int CODEC, bool STATS, int NCH, int OCT0, int AM, bool U8 = false>
 mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
-    auto kern = mc_decode_kernel<G, KW, CODEC, STATS, NCH, OCT0, AM>;
+    auto kern = mc_decode_kernel<G, KW, CODEC, STATS, NCH, OCT0, AM, U8>;
     constexpr uint32_t NG = 32 / G;
     const size_t warp_smem = NG * grp_smem;
     // warps per CTA: 8, fewer when a warp's staging buffers are large (Ṽ=T̃=256, 24-bit)
@@ -1044,6 +1051,11 @@ template <int CODEC, bool STATS, int NCH, int OCT0, int AM>
 mc_status launch_t(const Params& P, size_t grp_smem, cudaStream_t s) {
     // flag words per topology iteration: every word of a T~-triangle meshlet at once
     // (MC_WORD_STEP / MC_WORD_STEP32), one word when T~ <= 32 (no empty words)
+    // u8x4 output with a compile-time layout and halfword attributes: the u8x4-only kernel
+    // (strip codecs only: Basic measured 1% slower with it)
+    if constexpr (!STATS && NCH > 0 && AM == 0 && MC_U8_KERNEL && CODEC != MC_CODEC_BASIC)
+        if (P.u8x4 && P.tmax > 32 && P.tmax <= MC_GROUP16_TMAX)
+            return launch_g<16, MC_WORD_STEP, CODEC, STATS, NCH, OCT0, AM, true>(P, grp_smem, s);
     if (P.tmax <= 32) return launch_g<16, 1, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
     if (P.tmax <= MC_GROUP16_TMAX) return launch_g<16, MC_WORD_STEP, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
     return launch_g<32, MC_WORD_STEP32, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
