@@ -37,7 +37,7 @@
 //   MC_MAX_CTAS_PER_SM  cap on resident CTAs per SM used to size the persistent grid
 //   MC_GROUP16_TMAX     two meshlets per warp (16-lane groups) when T~ <= this
 //   MC_DYNAMIC          interleaved claim counters (0 = static grid stride)
-//   MC_STATIC_BELOW     launches with fewer records per group use the static stride (0 = never)
+//   MC_STATIC_BELOW     launches with fewer records per group use the static-stride kernel (0 = never)
 //   MC_ST_CS            streaming (.cs) output stores
 //   MC_BANK_PAD         group smem stride = 16 (mod 32) words
 #include "../../include/mc.h"
@@ -59,8 +59,7 @@
 #define MC_GROUP16_TMAX 128
 #endif
 #ifndef MC_STATIC_BELOW
-#define MC_STATIC_BELOW 0   // records per group below which a launch uses the static grid stride
-                            // (8: cfg2 +20%, but the runtime test costs cfg4 0.8%; off by default)
+#define MC_STATIC_BELOW 8   // records per group below which a launch uses the static-stride kernel
 #endif
 #ifndef MC_DYNAMIC
 #define MC_DYNAMIC 128   // interleaved claim streams (0 = static grid stride)
@@ -243,7 +242,7 @@ constexpr int min_blocks() {
     return MC_MIN_BLOCKS > 1 ? MC_MIN_BLOCKS : 3;
 }
 
-template <int G, int KW, int CODEC, bool STATS, int NCH, int OCT0, int AM, bool U8 = false>
+template <int G, int KW, int CODEC, bool STATS, int NCH, int OCT0, int AM, bool U8 = false, bool ST = false>
 __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_kernel(const __grid_constant__ Params P) {
     static_assert(G == 8 || G == 16 || G == 32, "group size");
     constexpr bool B16 = AM == 0, VWK = AM == 2;
@@ -290,8 +289,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
     const uint32_t ngroups = gridDim.x * wpc * NG;
     uint32_t grabbed = 0;
     auto grab = [&]() -> uint32_t {
-        if (MC_STATIC_BELOW == 0 || P.ctr) return base0 + stream + NS * atomicAdd(P.ctr + stream, 1u);
-        return base0 + gg + (grabbed++) * ngroups;
+        if constexpr (!ST) return base0 + stream + NS * atomicAdd(P.ctr + stream, 1u);
+        else return base0 + gg + (grabbed++) * ngroups;
     };
 #else
     const uint32_t ngroups = gridDim.x * wpc * NG;
@@ -990,9 +989,9 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     return MC_OK;
 }
 
-template <int G, int KW, int CODEC, bool STATS, int NCH, int OCT0, int AM, bool U8 = false>
+template <int G, int KW, int CODEC, bool STATS, int NCH, int OCT0, int AM, bool U8 = false, bool ST = false>
 mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
-    auto kern = mc_decode_kernel<G, KW, CODEC, STATS, NCH, OCT0, AM, U8>;
+    auto kern = mc_decode_kernel<G, KW, CODEC, STATS, NCH, OCT0, AM, U8, ST>;
     constexpr uint32_t NG = 32 / G;
     const size_t warp_smem = NG * grp_smem;
     // warps per CTA: 8, fewer when a warp's staging buffers are large (Ṽ=T̃=256, 24-bit)
@@ -1031,7 +1030,7 @@ mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
     PL.ctr = nullptr;
 #if MC_DYNAMIC
-    if (P.list || (uint64_t)count >= (uint64_t)MC_STATIC_BELOW * grid * wpc * NG) {
+    if (!ST) {
         static uint32_t* slots = nullptr;
         static uint32_t seq = 0;
         std::lock_guard<std::mutex> g(mu);
@@ -1045,12 +1044,27 @@ mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
     return cudaGetLastError() == cudaSuccess ? MC_OK : MC_ERR_CUDA;
 }
 
+int device_sms() {
+    static int sms[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    return sms[dev] > 0 ? sms[dev] : 148;
+}
+
 // group size: two meshlets per warp (G = 16) when a meshlet has at most
 // MC_GROUP16_TMAX decoded triangles, else one meshlet per warp (G = 32)
 template <int CODEC, bool STATS, int NCH, int OCT0, int AM>
 mc_status launch_t(const Params& P, size_t grp_smem, cudaStream_t s) {
     // flag words per topology iteration: every word of a T~-triangle meshlet at once
     // (MC_WORD_STEP / MC_WORD_STEP32), one word when T~ <= 32 (no empty words)
+    // short launches (fewer than MC_STATIC_BELOW records per group of a full grid) of the
+    // u32 output with a compile-time halfword layout: the static-stride kernel (no claim
+    // counters, no memset; a separate kernel so the long launches pay no run-time test)
+    if constexpr (!STATS && NCH > 0 && AM == 0 && MC_DYNAMIC && MC_STATIC_BELOW > 0)
+        if (!P.list && !P.u8x4 && P.tmax > 32 && P.tmax <= MC_GROUP16_TMAX &&
+            (uint64_t)(P.end - P.first) < (uint64_t)MC_STATIC_BELOW * device_sms() * 3u * 16u)
+            return launch_g<16, MC_WORD_STEP, CODEC, STATS, NCH, OCT0, AM, false, true>(P, grp_smem, s);
     // u8x4 output with a compile-time layout and halfword attributes: the u8x4-only kernel
     // (strip codecs only: Basic measured 1% slower with it)
     if constexpr (!STATS && NCH > 0 && AM == 0 && MC_U8_KERNEL && CODEC != MC_CODEC_BASIC)
