@@ -26,9 +26,11 @@
  * explicit fmaf (FORMAT.md §3, §4.3).
  *
  * Parity status: sequential decode, restarts, reuse expansion,
- * quantiser and budgets are pinned by tests/test_oracle_*.py.  The octahedral
- * normal decode (or_oct_decode) is an extension the paper does not define:
- * "parity unpinned" by the paper; pinned only by closed-form special cases.
+ * quantiser and budgets are pinned by tests/test_oracle_*.py; the binary32
+ * dequantisation by tests/test_oracle_dequant.py (exact rationals).  The octahedral
+ * normal decode (or_oct_decode) is an extension the paper does not define (FORMAT.md
+ * §4.3, reading R13): pinned by closed-form special cases and by float64 error bounds
+ * (<= 4 ulp normalisation, <= 2^-21 absolute end to end), not by the paper.
  */
 #include <math.h>
 #include <stdint.h>

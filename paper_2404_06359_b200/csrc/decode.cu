@@ -76,6 +76,9 @@
 #ifndef MC_WORD_STEP32
 #define MC_WORD_STEP32 8 // flag words per topology iteration, 32-lane groups (T~ > 128)
 #endif
+#ifndef MC_OCT_DIV
+#define MC_OCT_DIV 0
+#endif
 #ifndef MC_MAX_CTAS_PER_SM
 #define MC_MAX_CTAS_PER_SM 64
 #endif
@@ -205,10 +208,16 @@ __device__ __forceinline__ void oct_decode(float ex, float ey, float& ox, float&
     const float x = z < 0.0f ? fx : ex, y = z < 0.0f ? fy : ey;
     const float s2 = __fmaf_rn(z, z, __fmaf_rn(y, y, __fmul_rn(x, x)));
     const float r = __fsqrt_rn(s2);
+#if MC_OCT_DIV
+    ox = __fdiv_rn(x, r);
+    oy = __fdiv_rn(y, r);
+    oz = __fdiv_rn(z, r);
+#else
     const float inv = __frcp_rn(r);
     ox = __fmul_rn(x, inv);
     oy = __fmul_rn(y, inv);
     oz = __fmul_rn(z, inv);
+#endif
 }
 
 struct WarpStats {

@@ -100,17 +100,19 @@ def test_layouts(mc, orc):
 # ------------------------------------------------------------------ exhaustive tiny streams
 
 def test_exhaustive_tiny_gts(mc, orc):
-    """Every GTS stream with T' <= 5 and V <= 6 (all flags x all indices), one launch."""
+    """Every GTS stream with T' <= 6 and V <= 6 (all flags x all indices, SURVEY §8(c)
+    "tiny meshlets"), one launch: 429,344 records."""
     ms = []
-    for Tp in range(1, 6):
+    for Tp in range(1, 7):
         for V in range(3, 7):
             for flags in itertools.product([0, 1], repeat=Tp - 1):
                 for idx in itertools.product(range(V), repeat=Tp - 1):
                     ms.append(gts_meshlet(V, flags, idx))
-    assert len(ms) > 30000
+    assert len(ms) == sum(2 ** (Tp - 1) * V ** (Tp - 1) for Tp in range(1, 7) for V in range(3, 7))
+    assert len(ms) > 400000
     rng = np.random.default_rng(0)
     codes = rng.integers(0, 256, size=sum(m["V"] for m in ms))
-    blob = pack_meshlets(orc, 1, ms, codes=codes, vmax=6, tmax=5)
+    blob = pack_meshlets(orc, 1, ms, codes=codes, vmax=6, tmax=6)
     gpu_vs_oracle(mc, orc, blob)
 
 

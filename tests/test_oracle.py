@@ -419,6 +419,63 @@ def test_oct_inverse_of_encode(orc):
     assert np.abs(np.linalg.norm(out.astype(np.float64), axis=1) - 1).max() < 3e-7
 
 
+def _oct_inputs():
+    """(ex, ey) pairs: uniform on [-1,1]^2, both octahedron halves, the 16-bit grid of
+    FORMAT.md §3 (q·Δ + g with Δ = 2/(2^16-1), g = -1), fold boundaries and tiny values."""
+    rng = np.random.default_rng(5)
+    u = rng.uniform(-1, 1, size=(20000, 2))
+    d, g = np.float32(2.0 / 65535.0), np.float32(-1.0)
+    qg = rng.integers(0, 65536, size=(20000, 2)).astype(np.float32)
+    grid = (qg * np.float64(d) + np.float64(g))            # values near the grid, any rounding
+    edge = np.array([[a, b] for a in (-1, -0.5, -1e-30, 0.0, 1e-30, 0.5, 1) for b in (-1, -0.75, 0.0, 0.25, 1)])
+    diag = np.stack([np.linspace(-1, 1, 4001), 1 - np.abs(np.linspace(-1, 1, 4001))], 1)   # z = 0 fold line
+    return np.concatenate([u, grid, edge, diag, -diag]).astype(np.float32)
+
+
+def test_oct_vs_float64_normalisation(orc):
+    """FORMAT.md §4.3 (R13) against float64 (no pin from the paper: the paper only cites
+    octahedral normals).  Error analysis of the binary32 sequence (u = 2^-24):
+    the fold rounds x, y once and z twice (absolute <= u each, values <= 1); the folded
+    vector has |v| >= 1/sqrt(3) (|x|+|y|+|z| = 1), so normalising amplifies that by
+    <= sqrt(3) (<= 2.1u); s2 (3 roundings incl. x*x) <= 2u relative, sqrt u, reciprocal u,
+    product u -> <= 4u relative on each component.  Bound: |n32 - n64| <= 2^-21 (= 8u)
+    absolute per component, where n64 = normalize(fold(ex, ey)) in float64."""
+    e = _oct_inputs()
+    out = np.array([orc.oct_decode(float(a), float(b)) for a, b in e], np.float64)
+    ex, ey = e[:, 0].astype(np.float64), e[:, 1].astype(np.float64)
+    z = 1 - np.abs(ex) - np.abs(ey)
+    sx, sy = np.where(ex >= 0, 1.0, -1.0), np.where(ey >= 0, 1.0, -1.0)
+    x = np.where(z < 0, (1 - np.abs(ey)) * sx, ex)
+    y = np.where(z < 0, (1 - np.abs(ex)) * sy, ey)
+    v = np.stack([x, y, z], 1)
+    n64 = v / np.linalg.norm(v, axis=1, keepdims=True)
+    err = np.abs(out - n64)
+    assert err.max() <= 2.0 ** -21, err.max()
+    # the fold branch is taken (z < 0) for a good share of the inputs, and z = 0 exactly on the diagonals
+    assert (z < 0).mean() > 0.3
+
+
+def test_oct_normalisation_ulp_bound(orc):
+    """The normalisation step alone: with the fold evaluated in binary32 (numpy float32
+    arithmetic is IEEE RN), each output component is within 4 ulp (binary32) of the
+    float64 quotient c / |v| of the same folded vector (the <= 4u relative bound above)."""
+    e = _oct_inputs()
+    out = np.array([orc.oct_decode(float(a), float(b)) for a, b in e], np.float32)
+    one = np.float32(1)
+    ex, ey = e[:, 0], e[:, 1]
+    ax, ay = np.abs(ex), np.abs(ey)
+    z = (one - ax) - ay
+    x = np.where(z < 0, (one - ay) * np.where(ex >= 0, one, -one), ex).astype(np.float32)
+    y = np.where(z < 0, (one - ax) * np.where(ey >= 0, one, -one), ey).astype(np.float32)
+    v = np.stack([x, y, z], 1).astype(np.float64)
+    q = v / np.linalg.norm(v, axis=1, keepdims=True)
+    ulp = np.spacing(np.abs(q).astype(np.float32)).astype(np.float64)
+    nz = q != 0
+    ulps = np.abs(out.astype(np.float64) - q)[nz] / ulp[nz]
+    assert ulps.max() <= 4.0, ulps.max()
+    assert np.all(out[~nz] == 0)          # exact zeros stay zero (x, y or z = 0)
+
+
 # ------------------------------------------------------------------ budgets (P:586-591, S:365-373)
 
 def test_bit_budgets(orc):
