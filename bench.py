@@ -1,25 +1,34 @@
 #!/usr/bin/env python
 """Benchmark: per-meshlet decompression (arXiv 2404.06359) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4_city] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4_city]
+                    [--scaling strong|weak] [--impl ours|reference]
 
 One STEP = one decode of the rank's whole shard of the scene (every §8(a) row:
 record staging, index expansion, L/R lookback, triangle assembly, attribute unpack +
 dequantisation, index and vertex stores) = one launch of the sm_100a kernel.
 
 Default workload (N=1): BASELINE cfg4, the instanced synthetic city, 1000 instances of
-16 seeded buildings x 99,372 tris = 99.4M triangles per GPU, 64v/126t meshlets,
-GTS-Reuse, pos3 + oct2 + uv2 at 16 bits.  At N>1 every rank decodes its own
-1000-instance shard of an N x 1000-instance city (weak scaling; no data-path
-collective; one NCCL all-reduce of the checksum after timing).
+16 seeded buildings x 99,372 tris = 99.4M triangles, 64v/126t meshlets, GTS-Reuse,
+pos3 + oct2 + uv2 at 16 bits.  Multi-GPU (torchrun, one rank per GPU), no data-path
+collective (meshlets are independent):
+  --scaling strong (default): the SAME 1000-instance city split over the N ranks by
+      instance ranges (global output bases); value = the scene's triangles / max-rank time;
+  --scaling weak: every rank decodes its own 1000-instance shard of an N x 1000 city.
+One NCCL all-reduce of the checksums after timing (FORMAT.md §6).
 
-Inputs (~1 GB compressed) and outputs (~3.6 GB) are far larger than the 126 MB L2, so
-no L2 flush is needed between steps; the smaller parity workloads (--workload cfg1-3,
-working set < 4 x L2) flush L2 between steps and time the sum of the launches.  Timing:
-CUDA events on the launching stream, barrier + synchronize on both sides, max over ranks.
+Timing: W eager warm-up steps, then the K steps are captured in ONE CUDA graph with an
+external CUDA event around every launch (the per-launch durations give the roofline and
+the median / p10 / p90); the graph is replayed once untimed, then once timed, bracketed by
+barrier + synchronize on both sides, max over ranks.  cfg4 moves 4.6 GB per step (>> the
+126 MB L2): no flush.  Workloads under 4 x L2 (cfg1-cfg3) get a 2 x L2 memset between
+steps (inside the graph, outside the per-launch events) and are timed as the sum of the
+launches.
 
-Prints ONE JSON line on rank 0.  ``--impl reference`` times the oracle (plain-C
-sequential decoder, ``oracle/``) on the host cores instead.
+At N = 1 the cpu_baseline leg times the oracle (plain-C sequential decoder, oracle/) on the
+host cores over the workload and checks the GPU checksums against the oracle's decode of
+the whole workload ("parity").  ``--impl reference`` times the oracle alone (the base
+contract's reference arm for this tier).  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -48,8 +57,7 @@ WORKLOADS = {
     "cfg1_grid": dict(desc="32x32 quad grid, 2,048 tris, pos3+nrm3+uv2 @16b", vmax=64, tmax=126),
     "cfg2_torus": dict(desc="torus 1000x500, 1M tris, pos3 @16b", vmax=64, tmax=126),
     "cfg3_sphere": dict(desc="displaced cube-sphere 12*913^2 = 10.0M tris, pos3+oct2+uv2 @16b", vmax=64, tmax=126),
-    "cfg4_city": dict(desc="instanced city, 1000 instances x 99,372 tris per GPU, pos3+oct2+uv2 @16b",
-                      vmax=64, tmax=126),
+    "cfg4_city": dict(desc="instanced city, 1000 instances x 99,372 tris, pos3+oct2+uv2 @16b", vmax=64, tmax=126),
     "cfg3_sphere_nrm8": dict(desc="cfg3 sphere with raw normals: pos3+nrm3+uv2 @16b (the paper's 8 attributes)",
                              vmax=64, tmax=126),
 }
@@ -61,17 +69,30 @@ def log(*a):
 
 # ----------------------------------------------------------------------------- scenes
 
+def split_range(total: int, rank: int, world: int):
+    """Contiguous [first, first+count) of `total` units for `rank` (first ranks take the remainder)."""
+    first = rank * total // world
+    return first, (rank + 1) * total // world - first
+
+
 def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: int, protos_k=(16, 91),
-               vw: bool = False, cull: bool = False):
-    """The rank's shard of the workload as a product-encoded blob (mc_encode path)."""
+               vw: bool = False, cull: bool = False, scaling: str = "strong"):
+    """The rank's shard of the workload as a product-encoded blob (mc_encode path).
+
+    cfg4: strong = instances [split of `instances`] of one `instances`-instance city;
+    weak = instances [rank*instances, (rank+1)*instances) of a world*instances city.
+    Shards keep the whole scene's global output bases, so per-rank checksums add up to
+    the scene's (FORMAT.md §6).  Other workloads: strong = byte-balanced record ranges
+    of the single mesh (mc_blob_shard_ranges), weak = a replica of the mesh per rank."""
     w = WORKLOADS[workload]
     if workload == "cfg4_city":
-        scene = synth.city(num_instances=instances * world, num_prototypes=protos_k[0], k=protos_k[1], seed=0)
+        total = instances if scaling == "strong" else instances * world
+        scene = synth.city(num_instances=total, num_prototypes=protos_k[0], k=protos_k[1], seed=0)
         protos = [mc.mc_encode(p, w["vmax"], w["tmax"], codec, variable_widths=vw, cull_cones=cull)
                   for p in scene.prototypes]
-        blob = mc.mc_blob_instance_range(protos, scene.instance_proto, scene.instance_offset,
-                                         rank * instances, instances)
-        meta = {"instances_per_gpu": instances, "prototypes": protos_k[0],
+        first, count = split_range(total, rank, world) if scaling == "strong" else (rank * instances, instances)
+        blob = mc.mc_blob_instance_range(protos, scene.instance_proto, scene.instance_offset, first, count)
+        meta = {"instances": total, "instances_this_rank": count, "prototypes": protos_k[0],
                 "restarts_per_meshlet": round(sum(p.encode_stats()["restarts"] for p in protos) /
                                               max(1, sum(p.layout.num_meshlets for p in protos)), 3)}
         return blob, meta
@@ -81,7 +102,7 @@ def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: 
             "cfg3_sphere_nrm8": lambda: synth.displaced_sphere(913, oct_normals=False)}[workload]()
     blob = mc.mc_encode(mesh, w["vmax"], w["tmax"], codec, variable_widths=vw, cull_cones=cull)
     meta = {"restarts_per_meshlet": round(blob.encode_stats()["restarts"] / max(1, blob.layout.num_meshlets), 3)}
-    if world > 1:   # strong-sharded replicas of the single mesh
+    if world > 1 and scaling == "strong":
         f, c = blob.shard_ranges(world)[rank]
         blob = blob.extract(f, c)
     return blob, meta
@@ -91,11 +112,34 @@ def record_real_triangles(data: np.ndarray, m0: int, m1: int) -> int:
     """Σ T = T' - 4R over records [m0, m1) read straight from FORMAT.md bytes."""
     off_dir = int(data[64:72].view(np.uint64)[0])
     off_rec = int(data[80:88].view(np.uint64)[0])
-    M = int(data[16:20].view(np.uint32)[0])
-    d = data[off_dir:off_dir + 4 * (M + 1)].view(np.uint32)[m0:m1].astype(np.int64) * 16 + off_rec
+    d = data[off_dir:off_dir + 4 * (m1 + 1)].view(np.uint32)[m0:m1].astype(np.int64) * 16 + off_rec
     tp = data[d + 9].astype(np.int64) + 1
     r = data[d + 12].astype(np.int64) | (data[d + 13].astype(np.int64) << 8)
     return int((tp - 4 * r).sum())
+
+
+def algorithmic_bytes(L, index_format: str, want_vertices: bool = True) -> int:
+    """compressed bytes read (records + directory + object table) + decompressed
+    bytes written (12 or 4 B per decoded triangle, 4 n_out B per vertex)."""
+    read = (L.total_bytes - L.off_rec) + 4 * (L.num_meshlets + 1) + 8 * L.n * L.num_objects
+    write = (4 if index_format == "u8x4" else 12) * L.total_tp + (4 * L.n_out * L.total_v if want_vertices else 0)
+    return int(read + write)
+
+
+def config_dict(args, L, meta, world: int, alg_bytes: int, flush: bool) -> dict:
+    """The `config` object, identical for both arms (ours and --impl reference)."""
+    w = WORKLOADS[args.workload]
+    return {"workload": args.workload, "desc": w["desc"], "codec": CODEC_NAMES[args.codec],
+            "index_format": args.index_format,
+            "attribute_widths": "per-meshlet (VW)" if args.variable_widths else "global b",
+            "compressed_bits_per_tri": round(8.0 * L.total_bytes / max(1, L.total_t), 3),
+            "meshlet": f"{w['vmax']}v/{w['tmax']}t", "scaling": args.scaling, "n_ranks": world,
+            "triangles_this_rank": int(L.total_t), "decoded_triangles_incl_degenerate_this_rank": int(L.total_tp),
+            "meshlets_this_rank": int(L.num_meshlets), "compressed_bytes_this_rank": int(L.total_bytes),
+            "l2": (f"L2 flushed between steps ({2 * L2_BYTES >> 20} MiB memset, outside the per-launch events; "
+                   f"working set {alg_bytes / 1e6:.0f} MB < 4 x L2); value from the summed per-launch events")
+            if flush else f"inputs+outputs ({alg_bytes / 1e9:.2f} GB) >> 126 MB L2 each step (no flush)",
+            **meta}
 
 
 def allreduce_u64_sum(values, dist, device):
@@ -116,30 +160,38 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
-def oracle_time(data: np.ndarray, seconds: float, cores: int):
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_time(data: np.ndarray, seconds: float, cores: int, checksum: bool = False):
     """Time the oracle decoder (as it stands) on `cores` host threads: passes over the
     first S records (S calibrated so one pass takes about `seconds`, capped at the whole
     workload), repeated until at least `seconds` of wall time have elapsed.
-    Returns (tri/s, S, T, wall, passes) with T the real triangles decoded over all passes."""
+    Returns (tri/s, S, T, wall, passes, cs) with T the real triangles decoded over all
+    passes and cs the FORMAT.md §6 checksums of the oracle's decode of the WHOLE workload
+    (records past S decoded once more after the timing) when `checksum`, else None."""
     import oracle
     info = oracle.blob_info(data)
     M = info.M
 
     # calibrate on one thread
     cal = min(M, 400)
-    tp_cal = 3 * 256 * cal
-    idx = np.zeros(tp_cal, np.uint32)
-    q = None
+    idx = np.zeros(3 * 256 * cal, np.uint32)
     f = np.zeros(info.n_out * 256 * cal, np.float32)
     t0 = time.perf_counter()
-    oracle.decode_range_raw(data, 0, cal, idx, q, f)
+    oracle.decode_range_raw(data, 0, cal, idx, None, f)
     per_rec = (time.perf_counter() - t0) / max(cal, 1)
     S = int(min(M, max(cal, seconds * cores / max(per_rec, 1e-9))))
-    # output buffers sized for records [0, S)
-    tot_tp = 3 * 256 * S if S < M else 3 * info.total_tp
-    tot_v = 256 * S if S < M else info.total_v
-    idx = np.zeros(min(tot_tp, 3 * info.total_tp), np.uint32)
-    f = np.zeros(info.n_out * min(tot_v, info.total_v), np.float32)
+    # output buffers for the whole workload (record outputs land at their blob positions)
+    idx = np.zeros(3 * info.total_tp, np.uint32)
+    f = np.zeros(info.n_out * info.total_v, np.float32)
     bounds = np.linspace(0, S, cores * 4 + 1).astype(np.int64)
     T1 = record_real_triangles(data, 0, S)
     passes = 0
@@ -151,9 +203,16 @@ def oracle_time(data: np.ndarray, seconds: float, cores: int):
             passes += 1
             if time.perf_counter() - t0 >= seconds or passes >= 10000:
                 break
-    wall = time.perf_counter() - t0
+        wall = time.perf_counter() - t0
+        cs = None
+        if checksum:
+            if S < M:   # the rest of the workload, once, untimed
+                rb = np.linspace(S, M, cores * 4 + 1).astype(np.int64)
+                list(ex.map(lambda i: oracle.decode_range_raw(data, int(rb[i]), int(rb[i + 1]), idx, None, f),
+                            range(len(rb) - 1)))
+            cs = [oracle.checksum(idx, 3 * info.base_tri), oracle.checksum(f, info.n_out * info.base_vtx)]
     T = T1 * passes
-    return T / wall, S, T, wall, passes
+    return T / wall, S, T, wall, passes, cs
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -183,17 +242,20 @@ class ClockSampler:
             log("clock sampler unavailable:", e)
         self._stop = threading.Event()
 
+    def _sample(self):
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
     def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.005)
+            self._sample()
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.ok:
@@ -205,6 +267,8 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.t.join()
+            if not self.samples:
+                self._sample()
 
     def summary(self):
         if not self.ok or not self.samples:
@@ -221,12 +285,17 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload: str):
+def ncu_traffic(workload: str, index_format: str, scaling: str, world: int):
+    """DRAM bytes per launch from the committed ncu --set full capture of this build
+    (profiles/ncu_summary.json, scripts/ncu_summary.py), for the same launch shape."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    key = workload + ("" if index_format == "u32" else "_" + index_format) + \
+        ("" if world == 1 or scaling == "weak" else f"_strong{world}")
     try:
-        return json.load(open(p))[workload]["dram_bytes_per_launch"]
+        e = json.load(open(p))[key]
+        return e["dram_bytes_per_launch"], e.get("report")
     except Exception:
-        return None
+        return None, None
 
 
 # ----------------------------------------------------------------------------- arms
@@ -238,29 +307,62 @@ def run_reference(args, rank, world):
     import oracle
     oracle.build()
     import paper_2404_06359_b200 as mc
-    blob, meta = build_blob(mc, args.workload, 0, 1, args.codec, args.instances, vw=args.variable_widths)
+    blob, meta = build_blob(mc, args.workload, 0, world, args.codec, args.instances, vw=args.variable_widths,
+                            scaling=args.scaling)
     data = np.array(blob.bytes)
+    L = blob.layout
+    alg = algorithmic_bytes(L, args.index_format)
     cores = host_cores()
     per_step = max(0.5, min(3.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         oracle_time(data, min(per_step, 1.0), cores)
-    rates, walls, tris, recs = [], [], 0, 0
+    walls, tris, recs, passes = [], 0, 0, 0
     for _ in range(args.steps):
-        r, S, T, wall, passes = oracle_time(data, per_step, cores)
-        rates.append(r)
+        r, S, T, wall, passes, _cs = oracle_time(data, per_step, cores)
         walls.append(wall)
         tris += T
         recs = S
     value = tris / sum(walls) / 1e9
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(walls) / len(walls),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/fp32",
-            "data": "synthetic", "config": {"workload": args.workload, **WORKLOADS[args.workload], **meta},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"per step: {passes} pass(es) over the first {recs} records of the workload "
-                                       f"(>= {per_step:.1f}s of CPU work)"},
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u32/fp32",
+            "data": "synthetic", "config": config_dict(args, L, meta, world, alg, alg < 4 * L2_BYTES),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
+                             "sample": f"per step: {passes} pass(es) over the first {recs} of {L.num_meshlets} "
+                                       f"records of rank 0's shard (>= {per_step:.1f}s of CPU work)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def time_steps(torch, step, steps: int, stream, flush_buf, use_graph: bool):
+    """Run `steps` steps on `stream`; returns (total_ms, per-launch ms array, mode).  With
+    use_graph the steps (and the L2 flush memsets) are captured in one CUDA graph with an
+    external timing event pair around every launch, replayed once untimed, then timed."""
+    ev = [(torch.cuda.Event(enable_timing=True, external=use_graph),
+           torch.cuda.Event(enable_timing=True, external=use_graph)) for _ in range(steps)]
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def body():
+        for k in range(steps):
+            if flush_buf is not None:
+                flush_buf.zero_()
+            ev[k][0].record()
+            step()
+            ev[k][1].record()
+
+    graph = None
+    if use_graph:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                body()
+            graph.replay()                     # untimed replay (uploads the graph)
+            torch.cuda.synchronize()
+        except Exception as e:                 # pragma: no cover - reported in the line
+            log("CUDA graph capture failed, timing eager launches:", repr(e))
+            graph = None
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    return graph, ev, g0, g1, body
 
 
 def run_ours(args, rank, world, local_rank):
@@ -275,58 +377,57 @@ def run_ours(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=dev)
     t0 = time.time()
     blob, meta = build_blob(mc, args.workload, rank, world, args.codec, args.instances, vw=args.variable_widths,
-                            cull=args.cull)
+                            cull=args.cull, scaling=args.scaling)
     L = blob.layout
     log(f"[rank {rank}] scene built in {time.time() - t0:.1f}s: {L.num_meshlets} meshlets, "
         f"T={L.total_t} T'={L.total_tp} V={L.total_v}, {L.total_bytes / 1e6:.1f} MB")
     db = mc.DeviceBlob(blob, device=dev, want_vertices=True, want_quantized=False, index_format=args.index_format)
-    stream = torch.cuda.current_stream(dev)
-    alg_bytes = db.algorithmic_bytes()
+    alg_bytes = algorithmic_bytes(L, args.index_format)
     view_dir = np.array([1.0, 2.0, -3.0], np.float64)
     view_dir = (view_dir / np.linalg.norm(view_dir)).astype(np.float32)
+    stream = torch.cuda.Stream(dev)
     if args.cull:   # FORMAT.md §7: one step = cull + scan + emit + decode of the visible records
-        step = lambda: db.decode_culled(view_dir, stream=stream)
+        step = lambda: db.decode_culled(view_dir)
         launches_per_step = 4
     else:
-        step = lambda: db.decode(stream=stream)
+        step = lambda: db.decode()
         launches_per_step = 1
 
-    # ---------------- device-resident timing (the headline `value`)
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # working sets under 4 x L2 (cfg1-cfg3) would be partly L2-resident from the previous
     # step: flush L2 between steps by writing a 2 x L2 buffer, outside the per-launch events,
     # and time the sum of the launches; cfg4 (4.6 GB per step) needs no flush
     flush = alg_bytes < 4 * L2_BYTES
     fbuf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if flush else None
-    with ClockSampler(torch, dev) as clk:
-        g0.record(stream)
-        for k in range(args.steps):
-            if flush:
-                fbuf.zero_()
-            ev[k][0].record(stream)
+
+    # ---------------- device-resident timing (the headline `value`)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
             step()
-            ev[k][1].record(stream)
-        g1.record(stream)
         torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
+        graph, ev, g0, g1, body = time_steps(torch, step, args.steps, stream, fbuf, not args.no_graph)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        with ClockSampler(torch, dev) as clk:
+            g0.record()
+            if graph is not None:
+                graph.replay()
+            else:
+                body()
+            g1.record()
+            torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
     launch_ms = np.array([a.elapsed_time(b) for a, b in ev])
     total_ms = float(launch_ms.sum()) if flush else g0.elapsed_time(g1)
-    tri_local = L.total_t
-    t = torch.tensor([total_ms, float(launch_ms.mean())], dtype=torch.float64, device=dev)
-    n = torch.tensor([float(tri_local), float(alg_bytes)], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, float(launch_ms.mean()), float(np.median(launch_ms))], dtype=torch.float64,
+                     device=dev)
+    n = torch.tensor([float(L.total_t), float(alg_bytes)], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(n, op=dist.ReduceOp.SUM)
-    max_ms, max_launch_ms = float(t[0]), float(t[1])
+    max_ms, max_launch_ms, max_median_ms = float(t[0]), float(t[1]), float(t[2])
     tri_all, bytes_all = float(n[0]), float(n[1])
     value = tri_all * args.steps / (max_ms * 1e-3) / 1e9
 
@@ -341,7 +442,8 @@ def run_ours(args, rank, world, local_rank):
                      "value_counts": "all scene triangles (culled ones included) per second"}
         alg_bytes = vis_bytes
     # ---------------- verification after timing: checksum all-reduce (the only collective)
-    st = db.decode_culled(view_dir, stream=stream, stats=True) if args.cull else db.decode_stats(stream=stream)
+    with torch.cuda.stream(stream):
+        st = db.decode_culled(view_dir, stats=True) if args.cull else db.decode_stats()
     checksum = allreduce_u64_sum([st["checksum_indices"], st["checksum_vertices"]], dist, dev)
     errs = torch.tensor([st["error_bits"]], dtype=torch.int64, device=dev)
     if dist:
@@ -356,9 +458,8 @@ def run_ours(args, rank, world, local_rank):
         h_idx = torch.empty(idx_words, dtype=torch.int32).pin_memory()
         h_v = torch.empty(L.n_out * L.total_v, dtype=torch.float32).pin_memory()
         ke = max(1, min(args.steps, args.e2e_steps))
-        for _ in range(1):
-            mc.mc_decode_host(L, h_blob, db.d_blob, h_idx, db.indices, h_v, db.vertices, flags=db.index_flags,
-                              stream=stream, chunks=args.e2e_chunks)
+        mc.mc_decode_host(L, h_blob, db.d_blob, h_idx, db.indices, h_v, db.vertices, flags=db.index_flags,
+                          stream=stream, chunks=args.e2e_chunks)
         torch.cuda.synchronize(dev)
         if dist:
             dist.barrier()
@@ -384,35 +485,38 @@ def run_ours(args, rank, world, local_rank):
         return
     peak, peak_src = peak_hbm()
     achieved = alg_bytes / (max_launch_ms * 1e-3) / 1e9
-    cpu = None
+    traffic, traffic_src = ncu_traffic(args.workload, args.index_format, args.scaling, world)
+    cpu, parity = None, None
     if not args.no_cpu_baseline and world == 1:
         import oracle
         oracle.build()
         cores = host_cores()
-        rate, S, T, wall, passes = oracle_time(np.array(blob.bytes), args.cpu_seconds, cores)
-        cpu = {"value": rate / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+        rate, S, T, wall, passes, cs = oracle_time(np.array(blob.bytes), args.cpu_seconds, cores,
+                                                   checksum=not args.cull)
+        cpu = {"value": rate / 1e9, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
                "sample": f"{passes} pass(es) over the first {S} of {L.num_meshlets} records "
                          f"({T} tris decoded in total), {wall:.1f}s wall on {cores} threads"}
+        if cs is not None:
+            parity = {"checked": f"FORMAT.md §6 checksums of the GPU decode vs the oracle's decode of all "
+                                 f"{L.num_meshlets} records of the workload",
+                      "indices": checksum[0] == cs[0], "vertices": checksum[1] == cs[1],
+                      "error_bits": int(errs.item()), "ok": checksum == cs and int(errs.item()) == 0}
+    q = np.percentile(launch_ms, [10, 50, 90])
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "u32/fp32", "data": "synthetic",
-        "config": {"workload": args.workload, "desc": WORKLOADS[args.workload]["desc"],
-                   "codec": CODEC_NAMES[args.codec], "index_format": args.index_format,
-                   "attribute_widths": "per-meshlet (VW)" if args.variable_widths else "global b",
-                   "compressed_bits_per_tri": round(8.0 * L.total_bytes / max(1, L.total_t), 3),
-                   "meshlet": f"{WORKLOADS[args.workload]['vmax']}v/{WORKLOADS[args.workload]['tmax']}t",
-                   "triangles_per_gpu": int(tri_local), "decoded_triangles_incl_degenerate_per_gpu": int(L.total_tp),
-                   "meshlets_per_gpu": int(L.num_meshlets), "compressed_bytes_per_gpu": int(L.total_bytes),
-                   "l2": (f"L2 flushed between steps ({2 * L2_BYTES >> 20} MiB memset, outside the timed launches; "
-                          f"working set {alg_bytes / 1e6:.0f} MB < 4 x L2); value from the summed per-launch events")
-                   if flush else f"inputs+outputs ({alg_bytes / 1e9:.2f} GB) >> 126 MB L2 each step (no flush)", **meta},
+        "config": config_dict(args, L, meta, world, alg_bytes, flush),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(args.workload), "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": int(alg_bytes),
-                     "launch_ms": max_launch_ms},
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": int(alg_bytes), "launch_ms": max_launch_ms},
+        "step_ms": {"p10": float(q[0]), "median": float(q[1]), "p90": float(q[2]), "mean": float(launch_ms.mean()),
+                    "max_rank_median": max_median_ms,
+                    "timing": ("one CUDA graph of the K steps, external events around each launch" if graph is not None
+                               else "eager launches, events around each launch")},
         "hbm_gbs_aggregate": bytes_all * args.steps / (max_ms * 1e-3) / 1e9,
         "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": e2e,
         "gpu_launches": args.steps * launches_per_step,
         "cull": cull_info,
@@ -431,6 +535,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=list(WORKLOADS), default="cfg4_city")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: one scene split over the ranks; weak: one scene shard per rank")
     ap.add_argument("--codec", type=int, default=2, choices=[1, 2, 3], help="1 GTS, 2 GTS-Reuse, 3 Basic")
     ap.add_argument("--cull", action="store_true",
                     help="cone-culled compacted decode (FORMAT.md §7, extension f2) for a fixed view direction")
@@ -438,7 +544,9 @@ def main():
                     help="per-meshlet attribute code widths (FORMAT.md VW, extension f1)")
     ap.add_argument("--index-format", default="u32", choices=["u32", "u8x4"],
                     help="u32: 3 global indices per triangle (default); u8x4: one local u8x4 word")
-    ap.add_argument("--instances", type=int, default=1000, help="cfg4 instances per GPU")
+    ap.add_argument("--instances", type=int, default=1000,
+                    help="cfg4 instances: of the whole scene (strong) or per rank (weak)")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--e2e-chunks", type=int, default=32, help="mc_decode_host pipeline depth (0/1 = serial)")

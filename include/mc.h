@@ -20,9 +20,14 @@
  *    mc_stats.error_bits (FORMAT.md §5) — the kernel never traps and never
  *    reads or writes outside the blob and the record's own output ranges.
  *  - Every function is thread-safe; mc_blob objects are immutable once built.
- *  - Each decode launch claims records from a block of device counters in the library
- *    (rotating over 64 blocks, zeroed on the launch's own stream): at most 64 decode
- *    launches may be in flight at once across all streams of a process.
+ *    Device state is per device: a call runs on the CURRENT CUDA device
+ *    (cudaSetDevice), which must own the device buffers it is given.
+ *  - Decode kernels claim records from a small device WORK buffer (claim counters):
+ *    the caller's mc_decode_args.d_work, or, when that is NULL, a block of a library
+ *    pool (64 blocks per device, handed out round robin by one sequence per device;
+ *    then at most 64 pool-backed decode launches may be in flight at once per device).
+ *    A work buffer is zero when a decode starts and zero again when it completes (the
+ *    decode's last CTA resets it), so no memset is enqueued per launch.
  */
 #ifndef MC_H
 #define MC_H
@@ -169,6 +174,9 @@ mc_status mc_blob_extract(const void *bytes, size_t n, uint32_t first, uint32_t 
                           mc_blob **out);
 
 /* ------------------------------------------------------------------ device decode */
+/* u32 words of a decode work buffer (mc_decode_args.d_work). */
+#define MC_DECODE_WORK_WORDS 256
+
 typedef struct {
     const mc_layout *layout;   /* host: mc_parse_header of the same blob                 */
     const void *d_blob;        /* device: the blob bytes (16-B aligned base)              */
@@ -179,6 +187,12 @@ typedef struct {
     float *d_vertices;         /* device or NULL: n_out*total_v fp32, FORMAT.md §4.2       */
     uint32_t *d_quantized;     /* device or NULL: n*total_v u32 grid values, §4.1          */
     uint32_t flags;            /* MC_DECODE_*                                             */
+    uint32_t *d_work;          /* device or NULL: MC_DECODE_WORK_WORDS u32 of claim-counter
+                                  scratch, caller-owned, zero-filled once before its first
+                                  use; every completed decode leaves it zero again, so
+                                  decodes ordered on one stream reuse it with no memset.
+                                  Two decodes in flight at the same time (different
+                                  streams) must not share one.  NULL = library pool.      */
 } mc_decode_args;
 
 /* Device statistics (FORMAT.md §5, §6), accumulated atomically. */
@@ -260,7 +274,8 @@ typedef struct {
 mc_status mc_decode_host(const mc_host_decode_args *args, void *stream);
 
 const char *mc_status_str(mc_status s);
-uint32_t mc_abi_version(void);   /* 3 (mc_encode_params.flags, mc_layout.flags, mc_host_decode_args.chunks) */
+uint32_t mc_abi_version(void);   /* 4 (3: mc_encode_params.flags, mc_layout.flags, mc_host_decode_args.chunks;
+                                    4: mc_decode_args.d_work) */
 
 #ifdef __cplusplus
 }

@@ -22,7 +22,8 @@ LIB_PATH = _build.LIB
 MC_CODEC_GTS, MC_CODEC_GTS_REUSE, MC_CODEC_BASIC = 1, 2, 3
 MC_DECODE_BLOB_LOCAL_INDICES, MC_DECODE_INDEX_LOCAL_U8X4 = 1, 2
 MC_ENCODE_VARIABLE_WIDTHS, MC_ENCODE_CULL_CONES = 1, 2
-ABI_VERSION = 3
+ABI_VERSION = 4
+MC_DECODE_WORK_WORDS = 256
 MC_DERR_RECORD, MC_DERR_COUNTS, MC_DERR_INDEX, MC_DERR_REUSE, MC_DERR_OBJECT = 1, 2, 4, 8, 16
 
 
@@ -55,7 +56,7 @@ class mc_decode_args(ctypes.Structure):
     _fields_ = [("layout", ctypes.POINTER(mc_layout)), ("d_blob", ctypes.c_void_p),
                 ("first", ctypes.c_uint32), ("count", ctypes.c_uint32),
                 ("d_indices", ctypes.c_void_p), ("d_vertices", ctypes.c_void_p),
-                ("d_quantized", ctypes.c_void_p), ("flags", ctypes.c_uint32)]
+                ("d_quantized", ctypes.c_void_p), ("flags", ctypes.c_uint32), ("d_work", ctypes.c_void_p)]
 
 
 class mc_host_decode_args(ctypes.Structure):
@@ -271,29 +272,46 @@ def _check_sizes(layout: mc_layout, d_blob, d_indices, d_vertices, d_quantized, 
             raise MCError(f"{name}: {t.numel() * t.element_size()} bytes < {n * esz} required")
 
 
-def mc_decode_meshlets(layout: mc_layout, d_blob, d_indices, d_vertices=None, d_quantized=None, first: int = 0,
-                       count: int | None = None, flags: int = 0, stream=None):
-    """Enqueue the decode of records [first, first+count) on `stream` (torch stream or None)."""
+def _device_of(t):
+    """torch.cuda.device guard for the tensor's device (the C ABI runs on the current device)."""
+    import torch
+    return torch.cuda.device(t.device)
+
+
+def _check_work(d_work):
+    if d_work is not None and d_work.numel() * d_work.element_size() < 4 * MC_DECODE_WORK_WORDS:
+        raise MCError(f"d_work: {d_work.numel() * d_work.element_size()} bytes < {4 * MC_DECODE_WORK_WORDS} required")
+
+
+def _args(layout, d_blob, d_indices, d_vertices, d_quantized, first, count, flags, d_work):
     _check_sizes(layout, d_blob, d_indices, d_vertices, d_quantized, flags)
+    _check_work(d_work)
     count = layout.num_meshlets - first if count is None else count
-    a = mc_decode_args(ctypes.pointer(layout), d_blob.data_ptr(), first, count, d_indices.data_ptr(),
-                       None if d_vertices is None else d_vertices.data_ptr(),
-                       None if d_quantized is None else d_quantized.data_ptr(), flags)
-    _check(lib().mc_decode_meshlets(ctypes.byref(a), _stream_handle(stream)), "mc_decode_meshlets")
+    return mc_decode_args(ctypes.pointer(layout), d_blob.data_ptr(), first, count, d_indices.data_ptr(),
+                          None if d_vertices is None else d_vertices.data_ptr(),
+                          None if d_quantized is None else d_quantized.data_ptr(), flags,
+                          None if d_work is None else d_work.data_ptr())
+
+
+def mc_decode_meshlets(layout: mc_layout, d_blob, d_indices, d_vertices=None, d_quantized=None, first: int = 0,
+                       count: int | None = None, flags: int = 0, stream=None, d_work=None):
+    """Enqueue the decode of records [first, first+count) on `stream` (torch stream or None);
+    d_work: optional zero-initialised int32 tensor of MC_DECODE_WORK_WORDS (include/mc.h)."""
+    a = _args(layout, d_blob, d_indices, d_vertices, d_quantized, first, count, flags, d_work)
+    with _device_of(d_blob):
+        _check(lib().mc_decode_meshlets(ctypes.byref(a), _stream_handle(stream)), "mc_decode_meshlets")
 
 
 def mc_stats_reset(d_stats, stream=None):
-    _check(lib().mc_stats_reset(_tptr(d_stats), _stream_handle(stream)), "mc_stats_reset")
+    with _device_of(d_stats):
+        _check(lib().mc_stats_reset(_tptr(d_stats), _stream_handle(stream)), "mc_stats_reset")
 
 
 def mc_decode_stats(layout: mc_layout, d_blob, d_indices, d_stats, d_vertices=None, d_quantized=None, first: int = 0,
-                    count: int | None = None, flags: int = 0, stream=None):
-    _check_sizes(layout, d_blob, d_indices, d_vertices, d_quantized, flags)
-    count = layout.num_meshlets - first if count is None else count
-    a = mc_decode_args(ctypes.pointer(layout), d_blob.data_ptr(), first, count, d_indices.data_ptr(),
-                       None if d_vertices is None else d_vertices.data_ptr(),
-                       None if d_quantized is None else d_quantized.data_ptr(), flags)
-    _check(lib().mc_decode_stats(ctypes.byref(a), _tptr(d_stats), _stream_handle(stream)), "mc_decode_stats")
+                    count: int | None = None, flags: int = 0, stream=None, d_work=None):
+    a = _args(layout, d_blob, d_indices, d_vertices, d_quantized, first, count, flags, d_work)
+    with _device_of(d_blob):
+        _check(lib().mc_decode_stats(ctypes.byref(a), _tptr(d_stats), _stream_handle(stream)), "mc_decode_stats")
 
 
 def read_stats(d_stats) -> dict:
@@ -314,7 +332,8 @@ def mc_decode_host(layout: mc_layout, h_blob, d_blob, h_indices, d_indices, h_ve
                             None if h_quantized is None else h_quantized.data_ptr(), d_indices.data_ptr(),
                             None if d_vertices is None else d_vertices.data_ptr(),
                             None if d_quantized is None else d_quantized.data_ptr(), flags, chunks)
-    _check(lib().mc_decode_host(ctypes.byref(a), _stream_handle(stream)), "mc_decode_host")
+    with _device_of(d_blob):
+        _check(lib().mc_decode_host(ctypes.byref(a), _stream_handle(stream)), "mc_decode_host")
 
 
 class DeviceBlob:
@@ -336,15 +355,18 @@ class DeviceBlob:
         self.vertices = torch.empty(L.n_out * L.total_v, dtype=torch.float32, device=device) if want_vertices else None
         self.quantized = torch.empty(L.n * L.total_v, dtype=torch.int32, device=device) if want_quantized else None
         self.stats = torch.zeros(STATS_BYTES, dtype=torch.uint8, device=device)
+        # claim-counter work buffer (include/mc.h d_work): zeroed once, left zeroed by every
+        # completed decode; decodes of this DeviceBlob must be ordered on one stream
+        self.work = torch.zeros(MC_DECODE_WORK_WORDS, dtype=torch.int32, device=device)
 
     def decode(self, stream=None, flags=0, first=0, count=None):
         mc_decode_meshlets(self.layout, self.d_blob, self.indices, self.vertices, self.quantized, first, count,
-                           flags | self.index_flags, stream)
+                           flags | self.index_flags, stream, d_work=self.work)
 
     def decode_stats(self, stream=None, flags=0, first=0, count=None) -> dict:
         mc_stats_reset(self.stats, stream)
         mc_decode_stats(self.layout, self.d_blob, self.indices, self.stats, self.vertices, self.quantized, first,
-                        count, flags | self.index_flags, stream)
+                        count, flags | self.index_flags, stream, d_work=self.work)
         return read_stats(self.stats)
 
     def decode_culled(self, view_dir, stream=None, flags=0, stats=False):
@@ -359,14 +381,16 @@ class DeviceBlob:
         _check_sizes(L, self.d_blob, self.indices, self.vertices, self.quantized, flags | self.index_flags)
         a = mc_decode_args(ctypes.pointer(L), self.d_blob.data_ptr(), 0, L.num_meshlets, self.indices.data_ptr(),
                            None if self.vertices is None else self.vertices.data_ptr(),
-                           None if self.quantized is None else self.quantized.data_ptr(), flags | self.index_flags)
+                           None if self.quantized is None else self.quantized.data_ptr(), flags | self.index_flags,
+                           self.work.data_ptr())
         d = (ctypes.c_float * 3)(*[float(x) for x in view_dir])
         if stats:
             mc_stats_reset(self.stats, stream)
-        _check(lib().mc_decode_culled(ctypes.byref(a), ctypes.cast(d, ctypes.c_void_p), self.cull_scratch.data_ptr(),
-                                      self.cull_scratch.numel(), self.cull_counts.data_ptr(),
-                                      self.stats.data_ptr() if stats else None, _stream_handle(stream)),
-               "mc_decode_culled")
+        with _device_of(self.d_blob):
+            _check(lib().mc_decode_culled(ctypes.byref(a), ctypes.cast(d, ctypes.c_void_p),
+                                          self.cull_scratch.data_ptr(), self.cull_scratch.numel(),
+                                          self.cull_counts.data_ptr(), self.stats.data_ptr() if stats else None,
+                                          _stream_handle(stream)), "mc_decode_culled")
         return read_stats(self.stats) if stats else None
 
     def read_cull_counts(self) -> dict:

@@ -46,7 +46,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #ifndef MC_MIN_BLOCKS
@@ -76,6 +78,12 @@
 #ifndef MC_WORD_STEP32
 #define MC_WORD_STEP32 8 // flag words per topology iteration, 32-lane groups (T~ > 128)
 #endif
+#ifndef MC_G8
+#define MC_G8 0      // 8-lane groups (four meshlets per warp) when T~ <= 32
+#endif
+#ifndef MC_K64
+#define MC_K64 0     // two flag words per topology iteration when T~ <= 64
+#endif
 #ifndef MC_OCT_DIV
 #define MC_OCT_DIV 0
 #endif
@@ -102,7 +110,8 @@ struct Params {
     uint32_t hdr_words;        // record header words (16 + 4n [+ n with VW] rounded to 16) / 4
     uint32_t vw;               // FORMAT.md VW: per-record attribute widths w_c after L_c
     const uint4* list;         // culled decode (FORMAT.md §7): visible records {m, VB, TB, 0}, or null
-    uint32_t* ctr;             // MC_DYNAMIC: this launch's claim counters (device, zeroed)
+    uint32_t* ctr;             // MC_DYNAMIC: this launch's claim counters + done counter (device,
+                               // zero at launch; the last CTA to finish zeroes them again)
     const uint32_t* list_count;// device count of list entries
     uint32_t buf_words;        // per-buffer words (max_rec/4 + 4)
     uint32_t vtx_stage_words;  // vmax*n_out + 8 for the generic layout, else 0
@@ -227,11 +236,13 @@ struct WarpStats {
 
 
 #if MC_DYNAMIC
-// Position counters for the claim streams: kCounterBlocks blocks of MC_DYNAMIC counters,
-// one block per launch, rotating (up to kCounterBlocks decode launches may be in flight
-// at once across streams; each launch zeroes its block on its own stream first).
+static_assert(MC_DYNAMIC + 1 <= MC_DECODE_WORK_WORDS, "claim counters + done counter fit the work buffer");
+// Library pool of work buffers for callers that pass no d_work (include/mc.h): one
+// sequence per device hands out kCounterBlocks blocks round robin.  Each block is zero
+// when its launch starts: device globals start zeroed and every launch leaves its block
+// zeroed (the last CTA to finish resets it), so no memset is enqueued.
 constexpr uint32_t kCounterBlocks = 64;
-__device__ uint32_t g_position_counters[kCounterBlocks * MC_DYNAMIC];
+__device__ uint32_t g_position_counters[kCounterBlocks * MC_DECODE_WORK_WORDS];
 #endif
 
 // ------------------------------------------------------------------ the kernel
@@ -813,6 +824,23 @@ __global__ void __launch_bounds__(kThreads, min_blocks<NCH, AM>()) mc_decode_ker
             atomicMax(&P.stats->max_lookback, ws.max_lb);
         }
     }
+#if MC_DYNAMIC
+    if constexpr (!ST) {
+        // leave the work buffer zeroed for the next launch on the stream: every CTA counts
+        // itself done after all of its groups stopped claiming; the last one resets the
+        // claim counters and the done counter (no memset launch per decode)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const uint32_t done = atomicAdd(P.ctr + MC_DYNAMIC, 1u);
+            if (done == gridDim.x - 1u) {
+                volatile uint32_t* c = P.ctr;
+                for (uint32_t i = 0; i <= MC_DYNAMIC; ++i) c[i] = 0u;
+                __threadfence();
+            }
+        }
+    }
+#endif
 }
 
 __global__ void stats_reset_kernel(mc_stats* s) {
@@ -968,6 +996,8 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     P.vw = L.flags & 1u;
     P.list = nullptr;
     P.list_count = nullptr;
+    if (reinterpret_cast<uintptr_t>(a->d_work) & 3u) return MC_ERR_ARG;
+    P.ctr = a->d_work;   // launch_g falls back to the library pool when null
     P.hdr_words = ((16u + 4u * L.n + (P.vw ? L.n : 0u) + 15u) & ~15u) / 4u;
     P.buf_words = L.max_record_bytes / 4u + 4u;
     P.vtx_stage_words = 0;
@@ -998,8 +1028,46 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     return MC_OK;
 }
 
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return -1;
+    return dev;
+}
+
+int device_sms() {
+    static std::atomic<int> sms[kMaxDevices] = {};
+    const int dev = current_device();
+    if (dev < 0) return 148;
+    int v = sms[dev].load();
+    if (!v) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        sms[dev].store(v);
+    }
+    return v;
+}
+
+#if MC_DYNAMIC
+// next block of the library work pool on device `dev` (one sequence per device, shared by
+// every kernel variant, so concurrent launches of different variants never share a block)
+uint32_t* pool_block(int dev) {
+    static std::atomic<uintptr_t> base[kMaxDevices] = {};
+    static std::atomic<uint32_t> seq[kMaxDevices] = {};
+    uintptr_t b = base[dev].load();
+    if (!b) {
+        void* p = nullptr;
+        if (cudaGetSymbolAddress(&p, g_position_counters) != cudaSuccess) return nullptr;
+        b = reinterpret_cast<uintptr_t>(p);
+        base[dev].store(b);
+    }
+    return reinterpret_cast<uint32_t*>(b) + (size_t)MC_DECODE_WORK_WORDS * (seq[dev].fetch_add(1) % kCounterBlocks);
+}
+#endif
+
 template <int G, int KW, int CODEC, bool STATS, int NCH, int OCT0, int AM, bool U8 = false, bool ST = false>
 mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
+    uint32_t* const work = P.ctr;   // the caller's work buffer (mc_decode_args.d_work), or null
     auto kern = mc_decode_kernel<G, KW, CODEC, STATS, NCH, OCT0, AM, U8, ST>;
     constexpr uint32_t NG = 32 / G;
     const size_t warp_smem = NG * grp_smem;
@@ -1008,57 +1076,46 @@ mc_status launch_g(const Params& P, size_t grp_smem, cudaStream_t s) {
     uint32_t wpc = (uint32_t)std::min<size_t>(kWarpsPerCta, std::max<size_t>(1, budget / warp_smem));
     const size_t smem = warp_smem * wpc + 128;
     if (smem > 227u * 1024u) return MC_ERR_LIMITS;
+    // per-device launch state (the current device is the launch's device): the dynamic
+    // smem opt-in is a per-device function attribute; occupancy is cached per
+    // (device, warps per CTA, smem bucket)
+    const int dev = current_device();
+    if (dev < 0) return MC_ERR_CUDA;
+    static std::atomic<uint64_t> configured{0};   // bit d: attribute set on device d
+    if (!((configured.load() >> dev) & 1u)) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227u * 1024u)) != cudaSuccess)
+            return MC_ERR_CUDA;
+        configured.fetch_or(1ull << dev);
+    }
     static std::mutex mu;
-    static size_t configured = 0;
-    static int sms = 0;
-    static int bps_cache[kWarpsPerCta + 1][64] = {};
+    static std::unordered_map<uint64_t, int> bps_cache;
+    const uint64_t key = ((uint64_t)dev << 32) | ((uint64_t)wpc << 16) | std::min<size_t>(0xFFFF, smem / 1024);
+    int bps = 0;
     {
         std::lock_guard<std::mutex> g(mu);
-        if (smem > configured) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227u * 1024u)) != cudaSuccess)
-                return MC_ERR_CUDA;
-            configured = 227u * 1024u;
-        }
-        if (!sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        }
+        auto it = bps_cache.find(key);
+        if (it != bps_cache.end()) bps = it->second;
     }
-    const size_t bucket = std::min<size_t>(63, smem / 4096);
-    int bps = bps_cache[wpc][bucket];
     if (!bps) {
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 32 * wpc, smem) != cudaSuccess) return MC_ERR_CUDA;
         if (bps < 1) return MC_ERR_LIMITS;
-        bps_cache[wpc][bucket] = bps;
+        std::lock_guard<std::mutex> g(mu);
+        bps_cache[key] = bps;
     }
     Params PL = P;
     const uint32_t count = P.end - P.first;
     const uint64_t want = (count + wpc * NG - 1) / (wpc * NG);
-    const uint64_t cap = (uint64_t)sms * std::min(bps, MC_MAX_CTAS_PER_SM);
+    const uint64_t cap = (uint64_t)device_sms() * std::min(bps, MC_MAX_CTAS_PER_SM);
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, cap));
     PL.ctr = nullptr;
 #if MC_DYNAMIC
     if (!ST) {
-        static uint32_t* slots = nullptr;
-        static uint32_t seq = 0;
-        std::lock_guard<std::mutex> g(mu);
-        if (!slots && cudaGetSymbolAddress(reinterpret_cast<void**>(&slots), g_position_counters) != cudaSuccess)
-            return MC_ERR_CUDA;
-        PL.ctr = slots + MC_DYNAMIC * (seq++ % kCounterBlocks);
-        if (cudaMemsetAsync(PL.ctr, 0, 4 * MC_DYNAMIC, s) != cudaSuccess) return MC_ERR_CUDA;
+        PL.ctr = work ? work : pool_block(dev);
+        if (!PL.ctr) return MC_ERR_CUDA;
     }
 #endif
     kern<<<grid, 32 * wpc, smem, s>>>(PL);
     return cudaGetLastError() == cudaSuccess ? MC_OK : MC_ERR_CUDA;
-}
-
-int device_sms() {
-    static int sms[64] = {};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
-    if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
-    return sms[dev] > 0 ? sms[dev] : 148;
 }
 
 // group size: two meshlets per warp (G = 16) when a meshlet has at most
@@ -1079,7 +1136,14 @@ mc_status launch_t(const Params& P, size_t grp_smem, cudaStream_t s) {
     if constexpr (!STATS && NCH > 0 && AM == 0 && MC_U8_KERNEL && CODEC != MC_CODEC_BASIC)
         if (P.u8x4 && P.tmax > 32 && P.tmax <= MC_GROUP16_TMAX)
             return launch_g<16, MC_WORD_STEP, CODEC, STATS, NCH, OCT0, AM, true>(P, grp_smem, s);
+#if MC_G8
+    if (P.tmax <= 32) return launch_g<8, 1, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
+#else
     if (P.tmax <= 32) return launch_g<16, 1, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
+#endif
+#if MC_K64
+    if (P.tmax <= 64) return launch_g<16, 2, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
+#endif
     if (P.tmax <= MC_GROUP16_TMAX) return launch_g<16, MC_WORD_STEP, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
     return launch_g<32, MC_WORD_STEP32, CODEC, STATS, NCH, OCT0, AM>(P, grp_smem, s);
 }
@@ -1192,7 +1256,6 @@ std::vector<HostChunk> plan_host_chunks(const mc_layout& L, const uint8_t* hb, u
 }
 
 // Library-owned copy streams and events of the pipelined host decode, one set per device.
-constexpr int kMaxDevices = 64;
 struct PipeRes {
     std::mutex mu;
     cudaStream_t in = nullptr, out = nullptr;
@@ -1298,7 +1361,7 @@ mc_status mc_decode_host(const mc_host_decode_args* h, void* stream) {
     if (ch.size() < 2) {   // serial: H2D, decode, D2H on `stream`
         if (cudaMemcpyAsync(h->d_blob, h->h_blob, L.total_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
             return MC_ERR_CUDA;
-        mc_decode_args a{h->layout, h->d_blob, 0, M, h->d_indices, h->d_vertices, h->d_quantized, h->flags};
+        mc_decode_args a{h->layout, h->d_blob, 0, M, h->d_indices, h->d_vertices, h->d_quantized, h->flags, nullptr};
         mc_status rc = launch(&a, nullptr, s);
         if (rc != MC_OK) return rc;
         if (cudaMemcpyAsync(h->h_indices, h->d_indices, ib * L.total_tp, cudaMemcpyDeviceToHost, s) != cudaSuccess)
@@ -1330,7 +1393,7 @@ mc_status mc_decode_host(const mc_host_decode_args* h, void* stream) {
             !ok(cudaEventRecord(R->in_done[c], R->in)) || !ok(cudaStreamWaitEvent(s, R->in_done[c], 0)))
             return MC_ERR_CUDA;
         mc_decode_args a{h->layout, h->d_blob, a0.first, a1.first - a0.first, h->d_indices, h->d_vertices,
-                         h->d_quantized, h->flags};
+                         h->d_quantized, h->flags, nullptr};
         mc_status rc = launch(&a, nullptr, s);
         if (rc != MC_OK) return rc;
         if (!ok(cudaEventRecord(R->dec_done[c], s)) || !ok(cudaStreamWaitEvent(R->out, R->dec_done[c], 0)))

@@ -525,7 +525,10 @@ struct Encoder {
         build_adjacency();
         uint32_t O = 1;
         if (mesh.object_of_triangle)
-            for (uint32_t t = 0; t < T; ++t) O = std::max(O, mesh.object_of_triangle[t] + 1);
+            for (uint32_t t = 0; t < T; ++t) {
+            if (mesh.object_of_triangle[t] >= 65536u) return MC_ERR_LIMITS;   // no +1 wrap at UINT32_MAX
+            O = std::max(O, mesh.object_of_triangle[t] + 1);
+        }
         if (O > 65536) return MC_ERR_LIMITS;
         std::vector<std::vector<uint32_t>> by_obj(O);
         for (uint32_t t = 0; t < T; ++t) by_obj[obj(t)].push_back(t);
@@ -711,7 +714,8 @@ mc_status serialise(Encoder& E, mc_blob& out) {
         }
     // guard: enlarge Δ minimally until every meshlet's code range fits b bits
     std::atomic<int> range_err{0};
-    for (int iter = 0; iter < 64; ++iter) {
+    bool still_bad = true;
+    for (int iter = 0; iter < 96 && still_bad; ++iter) {
         std::vector<uint8_t> bad(size_t(O) * n, 0);
         parallel_for(M, th, [&](size_t m) {
             for (uint32_t c = 0; c < n; ++c) {
@@ -728,11 +732,21 @@ mc_status serialise(Encoder& E, mc_blob& out) {
             }
         });
         if (range_err) return MC_ERR_RANGE;
-        bool any = false;
+        still_bad = false;
         for (size_t k = 0; k < bad.size(); ++k)
-            if (bad[k]) { delta[k] = std::nextafter(delta[k], INFINITY); any = true; }
-        if (!any) break;
+            if (bad[k]) {
+                still_bad = true;
+                // one ulp at a time first (the overflow is FP rounding, SPEC's guard); after
+                // 32 steps scale by (2^b - 1)/(2^b - 2) per step so the loop always ends
+                const uint32_t maxc = (1u << mesh.bits[k % n]) - 1u;
+                if (iter < 32 || maxc < 2) delta[k] = std::nextafter(delta[k], INFINITY);
+                else {
+                    float f = float(double(delta[k]) * double(maxc) / double(maxc - 1u));
+                    delta[k] = std::nextafter(f, INFINITY);
+                }
+            }
     }
+    if (still_bad) return MC_ERR_RANGE;   // never leave codes wider than b bits
     // layout
     std::vector<uint64_t> roff(M + 1, 0);
     uint64_t tv = 0, ttp = 0, tt = 0, maxrec = 0, rs = 0;
@@ -872,9 +886,16 @@ mc_status parse(const uint8_t* b, size_t nbytes, mc_layout* L) {
     if ((L->flags & 2u) && ((L->off_cull & 15) || L->off_cull < L->off_obj + 8ull * L->n * L->num_objects ||
                             L->off_cull + 16ull * L->num_meshlets > L->off_rec))
         return MC_ERR_FORMAT;
-    // the directory must stay inside the records section
+    // the directory must stay inside the records section and be non-decreasing (host
+    // helpers dereference and binary-search its entries: O(M), once per parse)
     uint32_t d0 = get32(b + L->off_dir), dM = get32(b + L->off_dir + 4ull * L->num_meshlets);
     if (d0 != 0 || L->off_rec + 16ull * dM > nbytes) return MC_ERR_FORMAT;
+    uint32_t prev = 0;
+    for (uint32_t m = 1; m <= L->num_meshlets; ++m) {
+        const uint32_t d = get32(b + L->off_dir + 4ull * m);
+        if (d < prev) return MC_ERR_FORMAT;
+        prev = d;
+    }
     return MC_OK;
 }
 
@@ -883,7 +904,7 @@ mc_status parse(const uint8_t* b, size_t nbytes, mc_layout* L) {
 // ================================================================= C ABI (host part)
 extern "C" {
 
-uint32_t mc_abi_version(void) { return 3; }
+uint32_t mc_abi_version(void) { return 4; }
 
 const char* mc_status_str(mc_status s) {
     switch (s) {

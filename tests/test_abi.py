@@ -29,7 +29,7 @@ def test_exports_every_declared_symbol(mc):
     L = mc.lib()
     for name in sorted(declared):
         assert hasattr(L, name), name
-    assert L.mc_abi_version() == 3
+    assert L.mc_abi_version() == 4
     out = os.popen(f"nm -D {mc.LIB_PATH}").read()
     for name in declared:
         assert re.search(rf"\bT {name}\b", out), name
@@ -218,3 +218,48 @@ def test_cull_tables_survive_extract_and_instances(mc, orc):
         s = np.array(b.extract(f0, c).bytes)
         d = _dirs(1, 1)[0]
         assert np.array_equal(orc.decode_culled(s, d)[1], orc.decode_culled(full, d)[1][f0:f0 + c])
+
+
+def test_parse_rejects_malformed_directory(mc):
+    """FORMAT.md §1.2: dir[0] = 0, entries non-decreasing, dir[M] inside the records.  A
+    blob whose middle entries decrease or run past dir[M] is refused by mc_parse_header,
+    so the host helpers (shards, extract, pipelined host decode) never dereference it."""
+    blob = mc.mc_encode(synth.quad_grid(16, 16), 64, 126, 2)
+    data = np.array(blob.bytes)
+    L = blob.layout
+    assert L.num_meshlets >= 4
+    mc.parse_header(data)
+    dir_off = int(L.off_dir)
+    d = data[dir_off:dir_off + 4 * (L.num_meshlets + 1)].view(np.uint32)
+    bad = data.copy()
+    bad[dir_off:dir_off + 4 * (L.num_meshlets + 1)].view(np.uint32)[2] = d[L.num_meshlets] + 5
+    with pytest.raises(mc.MCError, match="not a valid"):
+        mc.parse_header(bad)
+    bad = data.copy()
+    bad[dir_off:dir_off + 4 * (L.num_meshlets + 1)].view(np.uint32)[2] = d[1] - 1
+    with pytest.raises(mc.MCError, match="not a valid"):
+        mc.parse_header(bad)
+    with pytest.raises(mc.MCError):
+        mc.mc_blob_shard_ranges(bad, 2)
+    with pytest.raises(mc.MCError):
+        mc.mc_blob_extract(bad, 0, 2)
+
+
+def test_object_id_limits(mc):
+    """Object ids index the per-object grid table (u16 in the record header, FORMAT.md
+    §1.4): ids >= 65536 (including UINT32_MAX, where id + 1 wraps) are MC_ERR_LIMITS."""
+    m = synth.quad_grid(4, 4)
+    T = m.indices.shape[0]
+    for bad_id in (65536, 0xFFFFFFFF):
+        obj = np.zeros(T, np.uint32)
+        obj[3] = bad_id
+        m2 = synth.Mesh(m.indices, m.attributes, m.bits, m.semantic)
+        m2.object_of_triangle = obj
+        with pytest.raises(mc.MCError, match="limits"):
+            mc.mc_encode(m2)
+    obj = np.zeros(T, np.uint32)
+    obj[T // 2:] = 65535
+    m3 = synth.Mesh(m.indices, m.attributes, m.bits, m.semantic)
+    m3.object_of_triangle = obj
+    b = mc.mc_encode(m3)
+    assert b.layout.num_objects == 65536

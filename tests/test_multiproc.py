@@ -1,6 +1,8 @@
 """Multi-process (gloo, world size 2, CPU) check of the sharded path bench.py runs under
-torchrun: each rank builds its instance-range shard of the city, decodes it (here with the
-oracle, on CPU), and the checksum all-reduce reproduces the whole scene's checksum."""
+torchrun: each rank builds its instance-range shard of the city (strong: a split of one
+city; weak: its own block of an N-times larger city), decodes it (here with the oracle, on
+CPU; tests/test_gpu_multiproc.py runs the product), and the checksum all-reduce reproduces
+the whole scene's checksum."""
 import os
 import socket
 
@@ -21,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, scaling, q):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -29,7 +31,7 @@ def _worker(rank, world, port, q):
     import bench
     import oracle
     import paper_2404_06359_b200 as mc
-    blob, meta = bench.build_blob(mc, "cfg4_city", rank, world, 2, instances=3, protos_k=(2, 6))
+    blob, meta = bench.build_blob(mc, "cfg4_city", rank, world, 2, instances=3, protos_k=(2, 6), scaling=scaling)
     data = np.array(blob.bytes)
     err, errs, idx, qv, f = oracle.decode(data)
     L = blob.layout
@@ -41,14 +43,15 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_two_rank_shards_checksum_allreduce(orc):
+@pytest.mark.parametrize("scaling", ["strong", "weak"])
+def test_two_rank_shards_checksum_allreduce(orc, scaling):
     import bench
     import paper_2404_06359_b200 as mc
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, scaling, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=300) for _ in range(world))
@@ -56,7 +59,7 @@ def test_two_rank_shards_checksum_allreduce(orc):
         p.join(timeout=60)
         assert p.exitcode == 0
     # the whole scene, built once on one process
-    full, _ = bench.build_blob(mc, "cfg4_city", 0, 1, 2, instances=6, protos_k=(2, 6))
+    full, _ = bench.build_blob(mc, "cfg4_city", 0, 1, 2, instances=3 if scaling == "strong" else 6, protos_k=(2, 6))
     err, errs, idx, qv, f = orc.decode(np.array(full.bytes))
     L = full.layout
     want = [orc.checksum(idx, 0), orc.checksum(f, 0)]
