@@ -17,13 +17,13 @@ collective (meshlets are independent):
   --scaling weak: every rank decodes its own 1000-instance shard of an N x 1000 city.
 One NCCL all-reduce of the checksums after timing (FORMAT.md §6).
 
-Timing: W eager warm-up steps, then the K steps are captured in ONE CUDA graph with an
-external CUDA event around every launch (the per-launch durations give the roofline and
-the median / p10 / p90); the graph is replayed once untimed, then once timed, bracketed by
-barrier + synchronize on both sides, max over ranks.  cfg4 moves 4.6 GB per step (>> the
-126 MB L2): no flush.  Workloads under 4 x L2 (cfg1-cfg3) get a 2 x L2 memset between
-steps (inside the graph, outside the per-launch events) and are timed as the sum of the
-launches.
+Timing: W eager warm-up steps, then the K steps are captured in ONE CUDA graph, replayed
+once untimed, then once timed, bracketed by barrier + synchronize on both sides, max over
+ranks.  A second graph of the K steps with an external CUDA event pair around every launch,
+replayed right after, gives the per-launch kernel durations (roofline launch time, median /
+p10 / p90).  cfg4 moves 4.6 GB per step (>> the 126 MB L2): no flush.  Workloads under
+4 x L2 (cfg1-cfg3) get a 2 x L2 memset between steps (inside the evented graph, which is
+then the timed one, outside the per-launch events) and are timed as the sum of the launches.
 
 At N = 1 the cpu_baseline leg times the oracle (plain-C sequential decoder, oracle/) on the
 host cores over the workload and checks the GPU checksums against the oracle's decode of
@@ -334,35 +334,39 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def time_steps(torch, step, steps: int, stream, flush_buf, use_graph: bool):
-    """Run `steps` steps on `stream`; returns (total_ms, per-launch ms array, mode).  With
-    use_graph the steps (and the L2 flush memsets) are captured in one CUDA graph with an
-    external timing event pair around every launch, replayed once untimed, then timed."""
-    ev = [(torch.cuda.Event(enable_timing=True, external=use_graph),
-           torch.cuda.Event(enable_timing=True, external=use_graph)) for _ in range(steps)]
-    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+def capture_steps(torch, step, steps: int, stream, flush_buf, use_graph: bool, events: bool):
+    """Capture `steps` steps (and the L2 flush memsets) on `stream` in one CUDA graph, with
+    an external timing-event pair around every launch when `events`; the graph is replayed
+    once untimed (upload).  Returns (run, ev): run() replays it (or, without a graph,
+    launches the steps eagerly) and ev holds the per-launch event pairs (or [])."""
+    def make_events(external):
+        return [(torch.cuda.Event(enable_timing=True, external=external),
+                 torch.cuda.Event(enable_timing=True, external=external)) for _ in range(steps)] if events else []
+
+    ev = make_events(use_graph)
 
     def body():
         for k in range(steps):
             if flush_buf is not None:
                 flush_buf.zero_()
-            ev[k][0].record()
+            if ev:
+                ev[k][0].record()
             step()
-            ev[k][1].record()
+            if ev:
+                ev[k][1].record()
 
-    graph = None
     if use_graph:
         try:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=stream):
                 body()
-            graph.replay()                     # untimed replay (uploads the graph)
+            graph.replay()
             torch.cuda.synchronize()
+            return graph.replay, ev
         except Exception as e:                 # pragma: no cover - reported in the line
             log("CUDA graph capture failed, timing eager launches:", repr(e))
-            graph = None
-            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-    return graph, ev, g0, g1, body
+            ev = make_events(False)
+    return body, ev
 
 
 def run_ours(args, rank, world, local_rank):
@@ -400,25 +404,34 @@ def run_ours(args, rank, world, local_rank):
     fbuf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if flush else None
 
     # ---------------- device-resident timing (the headline `value`)
+    # The timed region replays one CUDA graph of the K steps.  Without a flush it holds only
+    # the K launches (value = K steps / its duration); a second graph with an external event
+    # pair around every launch, replayed right after, gives the per-launch durations (the
+    # roofline's launch time, p10/median/p90).  With a flush the timed graph is the evented
+    # one and value comes from the summed launches (the memsets are outside the events).
+    use_graph = not args.no_graph
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize(dev)
-        graph, ev, g0, g1, body = time_steps(torch, step, args.steps, stream, fbuf, not args.no_graph)
+        run_ev, ev = capture_steps(torch, step, args.steps, stream, fbuf, use_graph, events=True)
+        run_t = run_ev if flush else capture_steps(torch, step, args.steps, stream, None, use_graph, events=False)[0]
+        graph_used = use_graph and run_t is not None and getattr(run_t, "__self__", None) is not None
         if dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
         with ClockSampler(torch, dev) as clk:
             g0.record()
-            if graph is not None:
-                graph.replay()
-            else:
-                body()
+            run_t()
             g1.record()
             torch.cuda.synchronize(dev)
         if dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
+        if not flush:        # per-launch durations, right after the timed region
+            run_ev()
+            torch.cuda.synchronize(dev)
     launch_ms = np.array([a.elapsed_time(b) for a, b in ev])
     total_ms = float(launch_ms.sum()) if flush else g0.elapsed_time(g1)
     t = torch.tensor([total_ms, float(launch_ms.mean()), float(np.median(launch_ms))], dtype=torch.float64,
@@ -512,8 +525,10 @@ def run_ours(args, rank, world, local_rank):
                      "algorithmic_bytes_per_launch": int(alg_bytes), "launch_ms": max_launch_ms},
         "step_ms": {"p10": float(q[0]), "median": float(q[1]), "p90": float(q[2]), "mean": float(launch_ms.mean()),
                     "max_rank_median": max_median_ms,
-                    "timing": ("one CUDA graph of the K steps, external events around each launch" if graph is not None
-                               else "eager launches, events around each launch")},
+                    "timing": (("timed: one CUDA graph of the K launches; per-launch: a second graph with external "
+                                "events around each launch, replayed right after" if not flush else
+                                "timed: one CUDA graph of the K launches + L2 flushes, external events around each "
+                                "launch") if graph_used else "eager launches, events around each launch")},
         "hbm_gbs_aggregate": bytes_all * args.steps / (max_ms * 1e-3) / 1e9,
         "cpu_baseline": cpu,
         "parity": parity,

@@ -173,6 +173,43 @@ mc_status mc_blob_shard_ranges(const void *bytes, size_t n, uint32_t parts, uint
 mc_status mc_blob_extract(const void *bytes, size_t n, uint32_t first, uint32_t count,
                           mc_blob **out);
 
+/* Blob summary (mc_blob_info): section sizes, counts and bit budgets. */
+typedef struct {
+    uint32_t codec, n, num_meshlets, num_objects;
+    uint64_t total_v, total_tp, total_t;  /* Σ V, Σ T' (decoded), Σ T (real)                    */
+    uint64_t restarts;                    /* Σ R over the record headers (T' = T + 4R)    */
+    uint64_t header_bytes, directory_bytes, object_bytes, cull_bytes, record_bytes, total_bytes;
+    uint64_t record_header_bytes;         /* Σ record headers (vtx/tri base, V, T', L_c [, w_c])  */
+    uint64_t flag_bytes;                  /* Σ L/R (+ increment) flag words           */
+    uint64_t index_bytes;                 /* Σ index (GTS), reuse (GTS-Reuse) or local-triangle
+                                             (Basic) bytes                                        */
+    uint64_t attribute_bytes;             /* Σ ceil(V·S/8): the packed attribute bits              */
+    uint64_t padding_bytes;               /* the rest of the records (16-B alignment)              */
+    double bits_per_triangle;             /* 8·total_bytes / Σ T                                   */
+    double index_bits_per_triangle;       /* 8·(flag + index bytes) / Σ T (Table 2's index buffer) */
+} mc_info;
+
+/* The global quantisation grid of one channel of one object, measured on the
+ * blob's own grid values q = L_c + code: */
+typedef struct {
+    float delta;        /* Δ_c, the grid spacing, as stored (fp32)                       */
+    float origin;       /* g_c, the grid origin (reading R9)                                     */
+    uint32_t bits;      /* b_c                                                           */
+    uint32_t w_steps;   /* largest meshlet extent in grid steps: max over the object's meshlets
+                           of max(code); <= 2^b - 1                            */
+    uint64_t W_steps;   /* global extent in grid steps: max q - min q over the object    */
+    double w;           /* w_c = w_steps · Δ_c, the largest meshlet extent               */
+    double W;           /* W_c = W_steps · Δ_c, the global mesh extent                   */
+    double info_bits;   /* information content log2(W_c / Δ_c) = log2(W_steps), 0 if 0  */
+} mc_channel_grid;
+
+/* Summarise a blob (host bytes): *out, and, when grids != NULL, the grid of every channel
+ * of every object, object-major: grids[o*n + c] for o < num_objects, c < n (grids_len >=
+ * num_objects*n entries, else MC_ERR_ARG).  One pass over the records (the attribute bits
+ * are unpacked on the host).  Errors: MC_ERR_FORMAT (not a valid blob or a record whose
+ * sections overrun it), MC_ERR_ARG. */
+mc_status mc_blob_info(const void *bytes, size_t n, mc_info *out, mc_channel_grid *grids, uint32_t grids_len);
+
 /* ------------------------------------------------------------------ device decode */
 /* u32 words of a decode work buffer (mc_decode_args.d_work). */
 #define MC_DECODE_WORK_WORDS 256

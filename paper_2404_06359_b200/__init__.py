@@ -73,11 +73,26 @@ class mc_stats(ctypes.Structure):
                [(k, ctypes.c_uint32) for k in ("max_lookback", "error_bits", "first_bad_meshlet", "num_bad")]
 
 
+class mc_info(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in ("codec", "n", "num_meshlets", "num_objects")] + \
+               [(k, ctypes.c_uint64) for k in
+                ("total_v", "total_tp", "total_t", "restarts", "header_bytes", "directory_bytes", "object_bytes",
+                 "cull_bytes", "record_bytes", "total_bytes", "record_header_bytes", "flag_bytes", "index_bytes",
+                 "attribute_bytes", "padding_bytes")] + \
+               [("bits_per_triangle", ctypes.c_double), ("index_bits_per_triangle", ctypes.c_double)]
+
+
+class mc_channel_grid(ctypes.Structure):
+    _fields_ = [("delta", ctypes.c_float), ("origin", ctypes.c_float), ("bits", ctypes.c_uint32),
+                ("w_steps", ctypes.c_uint32), ("W_steps", ctypes.c_uint64), ("w", ctypes.c_double),
+                ("W", ctypes.c_double), ("info_bits", ctypes.c_double)]
+
+
 STATS_BYTES = ctypes.sizeof(mc_stats)
 EXPORTS = ["mc_encode", "mc_blob_instance", "mc_blob_instance_range", "mc_blob_from_bytes", "mc_blob_bytes", "mc_blob_source_map",
            "mc_blob_encode_stats", "mc_blob_free", "mc_parse_header", "mc_blob_shard_ranges", "mc_blob_extract",
            "mc_decode_meshlets", "mc_decode_stats", "mc_stats_reset", "mc_decode_host", "mc_status_str",
-           "mc_abi_version", "mc_decode_culled", "mc_decode_culled_scratch_bytes"]
+           "mc_abi_version", "mc_decode_culled", "mc_decode_culled_scratch_bytes", "mc_blob_info"]
 
 _lib = None
 
@@ -116,6 +131,7 @@ def lib() -> ctypes.CDLL:
         L.mc_decode_culled.argtypes = [ctypes.POINTER(mc_decode_args), P, P, sz, P, P, P]
         L.mc_decode_culled_scratch_bytes.argtypes = [ctypes.POINTER(mc_layout)]
         L.mc_decode_culled_scratch_bytes.restype = sz
+        L.mc_blob_info.argtypes = [P, sz, ctypes.POINTER(mc_info), P, u32]
         _lib = L
     return _lib
 
@@ -189,6 +205,9 @@ class Blob:
     def extract(self, first: int, count: int) -> "Blob":
         return mc_blob_extract(self.bytes, first, count)
 
+    def info(self, grids: bool = True):
+        return mc_blob_info(self.bytes, grids)
+
 
 def parse_header(data: np.ndarray) -> mc_layout:
     L = mc_layout()
@@ -241,6 +260,24 @@ def mc_blob_shard_ranges(data: np.ndarray, parts: int):
     count = np.zeros(parts, np.uint32)
     _check(lib().mc_blob_shard_ranges(_p(data), data.nbytes, parts, _p(first), _p(count)), "mc_blob_shard_ranges")
     return [(int(f), int(c)) for f, c in zip(first, count)]
+
+
+def mc_blob_info(data: np.ndarray, grids: bool = True):
+    """Blob summary (dict of mc_info) and, with `grids`, the per-object per-channel grids
+    (list over objects of lists over channels of dicts of mc_channel_grid)."""
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    L = parse_header(data)
+    info = mc_info()
+    arr = (mc_channel_grid * max(1, L.num_objects * L.n))() if grids else None
+    _check(lib().mc_blob_info(_p(data), data.nbytes, ctypes.byref(info),
+                              ctypes.cast(arr, ctypes.c_void_p) if grids else None,
+                              L.num_objects * L.n if grids else 0), "mc_blob_info")
+    d = {k: getattr(info, k) for k, _ in mc_info._fields_}
+    if not grids:
+        return d, None
+    g = [[{k: getattr(arr[o * L.n + c], k) for k, _ in mc_channel_grid._fields_} for c in range(L.n)]
+         for o in range(L.num_objects)]
+    return d, g
 
 
 def mc_blob_extract(data: np.ndarray, first: int, count: int) -> Blob:

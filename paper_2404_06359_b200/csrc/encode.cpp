@@ -1067,6 +1067,105 @@ mc_status mc_blob_extract(const void* bytes, size_t n, uint32_t first, uint32_t 
     return MC_OK;
 }
 
+mc_status mc_blob_info(const void* bytes, size_t nbytes, mc_info* out, mc_channel_grid* grids, uint32_t grids_len) {
+    mc_layout L;
+    const uint8_t* b = static_cast<const uint8_t*>(bytes);
+    mc_status st = parse(b, nbytes, &L);
+    if (st != MC_OK) return st;
+    if (!out) return MC_ERR_ARG;
+    const uint32_t n = L.n, M = L.num_meshlets, O = L.num_objects;
+    const bool vw = L.flags & 1u;
+    if (grids && uint64_t(grids_len) < uint64_t(O) * n) return MC_ERR_ARG;
+    const uint32_t hdr = uint32_t(round16(16 + 4ull * n + (vw ? n : 0)));
+    std::memset(out, 0, sizeof(*out));
+    out->codec = L.codec;
+    out->n = n;
+    out->num_meshlets = M;
+    out->num_objects = O;
+    out->total_v = L.total_v;
+    out->total_tp = L.total_tp;
+    out->total_t = L.total_t;
+    out->header_bytes = kHeaderBytes;
+    out->directory_bytes = L.off_obj - L.off_dir;
+    out->object_bytes = ((L.flags & 2u) ? L.off_cull : L.off_rec) - L.off_obj;
+    out->cull_bytes = (L.flags & 2u) ? L.off_rec - L.off_cull : 0;
+    out->record_bytes = L.total_bytes - L.off_rec;
+    out->total_bytes = L.total_bytes;
+    // per record: section sizes (FORMAT.md §1.4) and, per channel, the largest code and
+    // the lowest / highest grid value q = L_c + code
+    std::vector<uint64_t> lo(size_t(O) * n, UINT64_MAX), hi(size_t(O) * n, 0);
+    std::vector<uint32_t> wmax(size_t(O) * n, 0);
+    std::vector<uint32_t> code_max(n);
+    for (uint32_t m = 0; m < M; ++m) {
+        const uint64_t r0 = L.off_rec + 16ull * get32(b + L.off_dir + 4ull * m);
+        const uint64_t r1 = L.off_rec + 16ull * get32(b + L.off_dir + 4ull * (m + 1));
+        if (r1 < r0 + hdr) return MC_ERR_FORMAT;
+        const uint32_t V = uint32_t(b[r0 + 8]) + 1, Tp = uint32_t(b[r0 + 9]) + 1, obj = get16(b + r0 + 10);
+        if (obj >= O) return MC_ERR_FORMAT;
+        out->restarts += get16(b + r0 + 12);
+        const uint32_t W = L.codec == MC_CODEC_BASIC ? 0u : (Tp + 31) / 32;
+        const uint64_t flag_b = 4ull * W * (L.codec == MC_CODEC_GTS_REUSE ? 2 : 1);
+        const uint64_t nb = L.codec == MC_CODEC_GTS ? Tp - 1ull
+                            : L.codec == MC_CODEC_BASIC ? 3ull * Tp
+                            : (V >= 3 && V - 3 <= Tp - 1 ? (Tp - 1ull) - (V - 3ull) : 0);
+        uint32_t S = 0;
+        uint8_t wd[16];
+        for (uint32_t c = 0; c < n; ++c) {
+            wd[c] = vw ? b[r0 + 16 + 4 * n + c] : L.bits[c];
+            if (wd[c] > L.bits[c]) return MC_ERR_FORMAT;
+            S += wd[c];
+        }
+        const uint64_t at = r0 + hdr + flag_b + ((nb + 3) & ~3ull);
+        const uint64_t at_b = (uint64_t(V) * S + 31) / 32 * 4;
+        if (at + at_b > r1) return MC_ERR_FORMAT;
+        out->record_header_bytes += hdr;
+        out->flag_bytes += flag_b;
+        out->index_bytes += nb;
+        out->attribute_bytes += (uint64_t(V) * S + 7) / 8;
+        // little-endian bit string of V records of S bits (FORMAT.md §1.4)
+        std::fill(code_max.begin(), code_max.end(), 0u);
+        uint64_t bit = 0;
+        for (uint32_t v = 0; v < V; ++v)
+            for (uint32_t c = 0; c < n; ++c) {
+                uint64_t word = 0;
+                const uint64_t byte0 = bit >> 3;
+                for (uint32_t k = 0; k < 5 && at + byte0 + k < r1; ++k) word |= uint64_t(b[at + byte0 + k]) << (8 * k);
+                const uint32_t code = wd[c] ? uint32_t((word >> (bit & 7)) & ((1ull << wd[c]) - 1)) : 0u;
+                code_max[c] = std::max(code_max[c], code);
+                bit += wd[c];
+            }
+        for (uint32_t c = 0; c < n; ++c) {
+            const size_t k = size_t(obj) * n + c;
+            const uint64_t Lc = get32(b + r0 + 16 + 4ull * c);
+            lo[k] = std::min(lo[k], Lc);
+            hi[k] = std::max(hi[k], Lc + code_max[c]);
+            wmax[k] = std::max(wmax[k], code_max[c]);
+        }
+    }
+    out->padding_bytes = out->record_bytes - out->record_header_bytes - out->flag_bytes - out->index_bytes -
+                         out->attribute_bytes;
+    out->bits_per_triangle = L.total_t ? 8.0 * double(L.total_bytes) / double(L.total_t) : 0.0;
+    out->index_bits_per_triangle = L.total_t ? 8.0 * double(out->flag_bytes + out->index_bytes) / double(L.total_t) : 0.0;
+    if (grids)
+        for (uint32_t o = 0; o < O; ++o)
+            for (uint32_t c = 0; c < n; ++c) {
+                const size_t k = size_t(o) * n + c;
+                mc_channel_grid& g = grids[k];
+                float d, org;
+                std::memcpy(&d, b + L.off_obj + 8ull * n * o + 4ull * c, 4);
+                std::memcpy(&org, b + L.off_obj + 8ull * n * o + 4ull * (n + c), 4);
+                g.delta = d;
+                g.origin = org;
+                g.bits = L.bits[c];
+                g.w_steps = wmax[k];
+                g.W_steps = lo[k] == UINT64_MAX ? 0 : hi[k] - lo[k];
+                g.w = double(g.w_steps) * double(d);
+                g.W = double(g.W_steps) * double(d);
+                g.info_bits = g.W_steps ? std::log2(double(g.W_steps)) : 0.0;
+            }
+    return MC_OK;
+}
+
 mc_status mc_blob_instance(const mc_blob* const* protos, uint32_t num_protos, const uint32_t* proto_of_instance,
                            const float* offset, uint32_t num_instances, mc_blob** out) {
     return mc_blob_instance_range(protos, num_protos, proto_of_instance, offset, num_instances, 0, num_instances, out);

@@ -263,3 +263,54 @@ def test_object_id_limits(mc):
     m3.object_of_triangle = obj
     b = mc.mc_encode(m3)
     assert b.layout.num_objects == 65536
+
+
+@pytest.mark.parametrize("codec,vw", [(1, False), (2, False), (3, False), (2, True)])
+def test_blob_info_against_oracle_decode(mc, orc, codec, vw):
+    """mc_blob_info (P:486-499 grid diagnostics, section sizes) against values computed
+    independently: grid extents from the ORACLE's decoded q values and the record fields
+    read by tests/streams.py; bit budgets restated from FORMAT.md §1.4."""
+    from streams import read_records
+    scene = synth.city(num_instances=3, num_prototypes=2, k=10, seed=4)
+    protos = [mc.mc_encode(p, 64, 126, codec, variable_widths=vw) for p in scene.prototypes]
+    blob = mc.mc_blob_instance(protos, scene.instance_proto, scene.instance_offset)
+    data = np.array(blob.bytes)
+    info, grids = blob.info()
+    L = blob.layout
+    err, errs, idx, q, f = orc.decode(data)
+    assert err == 0
+    recs = read_records(data)
+    n, O = L.n, L.num_objects
+    qv = q.reshape(-1, n).astype(np.int64)
+    lo = np.full((O, n), np.iinfo(np.int64).max)
+    hi = np.zeros((O, n), np.int64)
+    wmax = np.zeros((O, n), np.int64)
+    for r in recs:
+        sl = qv[r["vtx_base"]:r["vtx_base"] + r["V"]]
+        lo[r["object"]] = np.minimum(lo[r["object"]], sl.min(0))
+        hi[r["object"]] = np.maximum(hi[r["object"]], sl.max(0))
+        wmax[r["object"]] = np.maximum(wmax[r["object"]], (sl - np.array(r["L"], np.int64)).max(0))
+    off_obj = int(L.off_obj)
+    tab = data[off_obj:off_obj + 8 * n * O].view(np.float32).reshape(O, 2, n)
+    for o in range(O):
+        for c in range(n):
+            g = grids[o][c]
+            assert g["W_steps"] == hi[o, c] - lo[o, c] and g["w_steps"] == wmax[o, c]
+            assert g["w_steps"] <= (1 << g["bits"]) - 1          # b bits suffice (P:492)
+            assert g["delta"] == tab[o, 0, c] and g["origin"] == tab[o, 1, c]
+            assert g["info_bits"] == (np.log2(g["W_steps"]) if g["W_steps"] else 0.0)
+            assert abs(g["W"] - g["W_steps"] * float(tab[o, 0, c])) <= 1e-9 * max(1.0, g["W"])
+    # the largest meshlet extent spans the b-bit range (Δ = w/(2^b-1), P:488), non-VW grids
+    assert max(grids[o][c]["w_steps"] for o in range(O) for c in range(n)) >= (1 << 16) - 2
+    assert info["restarts"] == sum(r["R"] for r in recs)
+    assert info["total_t"] == L.total_t and info["num_meshlets"] == len(recs)
+    assert (info["header_bytes"] + info["directory_bytes"] + info["object_bytes"] + info["cull_bytes"] +
+            info["record_bytes"]) == info["total_bytes"] == data.nbytes
+    assert (info["record_header_bytes"] + info["flag_bytes"] + info["index_bytes"] + info["attribute_bytes"] +
+            info["padding_bytes"]) == info["record_bytes"]
+    W = [0 if codec == 3 else (r["Tp"] + 31) // 32 for r in recs]
+    assert info["flag_bytes"] == sum(4 * w * (2 if codec == 2 else 1) for w in W)
+    nb = [r["Tp"] - 1 if codec == 1 else 3 * r["Tp"] if codec == 3 else (r["Tp"] - 1) - (r["V"] - 3) for r in recs]
+    assert info["index_bytes"] == sum(nb)
+    assert info["attribute_bytes"] == sum((r["V"] * sum(r["widths"]) + 7) // 8 for r in recs)
+    assert abs(info["bits_per_triangle"] - 8 * data.nbytes / L.total_t) < 1e-9
