@@ -9,7 +9,7 @@ record staging, index expansion, L/R lookback, triangle assembly, attribute unpa
 dequantisation, index and vertex stores) = one launch of the sm_100a kernel.
 
 Default workload (N=1): BASELINE cfg4, the instanced synthetic city, 1000 instances of
-16 seeded buildings x 99,372 tris = 99.4M triangles, 64v/126t meshlets, GTS-Reuse,
+256 seeded buildings (12 k^2 tris, k in [81, 101]) = ~99.7M triangles, 64v/126t meshlets, GTS-Reuse,
 pos3 + oct2 + uv2 at 16 bits.  Multi-GPU (torchrun, one rank per GPU), no data-path
 collective (meshlets are independent):
   --scaling strong (default): the SAME 1000-instance city split over the N ranks by
@@ -19,11 +19,13 @@ One NCCL all-reduce of the checksums after timing (FORMAT.md §6).
 
 Timing: W eager warm-up steps, then the K steps are captured in ONE CUDA graph, replayed
 once untimed, then once timed, bracketed by barrier + synchronize on both sides, max over
-ranks.  A second graph of the K steps with an external CUDA event pair around every launch,
-replayed right after, gives the per-launch kernel durations (roofline launch time, median /
-p10 / p90).  cfg4 moves 4.6 GB per step (>> the 126 MB L2): no flush.  Workloads under
-4 x L2 (cfg1-cfg3) get a 2 x L2 memset between steps (inside the evented graph, which is
-then the timed one, outside the per-launch events) and are timed as the sum of the launches.
+ranks; the roofline's launch time is that region's time per step (it holds only the K
+decode launches).  After 0.5 s idle, K eager launches with a CUDA event pair around each
+give the per-launch distribution (median / p10 / p90).  Then the graph is replayed back to
+back for --sustained-seconds (`sustained`: this pool's B200s lower the SM clock under
+power management after ~0.1 s of full load; the K-step region is a burst).  cfg4 moves
+4.6 GB per step (>> the 126 MB L2): no flush.  Workloads under 4 x L2 (cfg1-cfg3) get a
+2 x L2 memset before each step and are timed as the sum of the evented eager launches.
 
 At N = 1 the cpu_baseline leg times the oracle (plain-C sequential decoder, oracle/) on the
 host cores over the workload and checks the GPU checksums against the oracle's decode of
@@ -57,7 +59,8 @@ WORKLOADS = {
     "cfg1_grid": dict(desc="32x32 quad grid, 2,048 tris, pos3+nrm3+uv2 @16b", vmax=64, tmax=126),
     "cfg2_torus": dict(desc="torus 1000x500, 1M tris, pos3 @16b", vmax=64, tmax=126),
     "cfg3_sphere": dict(desc="displaced cube-sphere 12*913^2 = 10.0M tris, pos3+oct2+uv2 @16b", vmax=64, tmax=126),
-    "cfg4_city": dict(desc="instanced city, 1000 instances x 99,372 tris, pos3+oct2+uv2 @16b", vmax=64, tmax=126),
+    "cfg4_city": dict(desc="instanced city, 1000 instances of 256 seeded buildings (~100k tris each), "
+                           "pos3+oct2+uv2 @16b", vmax=64, tmax=126),
     "cfg3_sphere_nrm8": dict(desc="cfg3 sphere with raw normals: pos3+nrm3+uv2 @16b (the paper's 8 attributes)",
                              vmax=64, tmax=126),
 }
@@ -75,7 +78,11 @@ def split_range(total: int, rank: int, world: int):
     return first, (rank + 1) * total // world - first
 
 
-def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: int, protos_k=(16, 91),
+CITY_PROTOTYPES = 256   # seeded buildings of the cfg4 city (each used by ~4 of the 1000 instances)
+CITY_K_JITTER = 10      # building subdivision k in [81, 101]: 78.7k..122.4k tris, ~99.8k on average
+
+
+def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: int, protos_k=(CITY_PROTOTYPES, 91),
                vw: bool = False, cull: bool = False, scaling: str = "strong"):
     """The rank's shard of the workload as a product-encoded blob (mc_encode path).
 
@@ -87,12 +94,15 @@ def build_blob(mc, workload: str, rank: int, world: int, codec: int, instances: 
     w = WORKLOADS[workload]
     if workload == "cfg4_city":
         total = instances if scaling == "strong" else instances * world
-        scene = synth.city(num_instances=total, num_prototypes=protos_k[0], k=protos_k[1], seed=0)
-        protos = [mc.mc_encode(p, w["vmax"], w["tmax"], codec, variable_widths=vw, cull_cones=cull)
-                  for p in scene.prototypes]
+        scene = synth.city(num_instances=total, num_prototypes=protos_k[0], k=protos_k[1], seed=0,
+                           k_jitter=CITY_K_JITTER if protos_k[0] > 8 else 0)
+        with ThreadPoolExecutor(min(32, host_cores())) as ex:   # independent meshes, one encoder thread each
+            protos = list(ex.map(lambda p: mc.mc_encode(p, w["vmax"], w["tmax"], codec, num_threads=1,
+                                                        variable_widths=vw, cull_cones=cull), scene.prototypes))
         first, count = split_range(total, rank, world) if scaling == "strong" else (rank * instances, instances)
         blob = mc.mc_blob_instance_range(protos, scene.instance_proto, scene.instance_offset, first, count)
         meta = {"instances": total, "instances_this_rank": count, "prototypes": protos_k[0],
+                "building_k": f"{protos_k[1]} +- {CITY_K_JITTER if protos_k[0] > 8 else 0}",
                 "restarts_per_meshlet": round(sum(p.encode_stats()["restarts"] for p in protos) /
                                               max(1, sum(p.layout.num_meshlets for p in protos)), 3)}
         return blob, meta
@@ -334,39 +344,33 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def capture_steps(torch, step, steps: int, stream, flush_buf, use_graph: bool, events: bool):
-    """Capture `steps` steps (and the L2 flush memsets) on `stream` in one CUDA graph, with
-    an external timing-event pair around every launch when `events`; the graph is replayed
-    once untimed (upload).  Returns (run, ev): run() replays it (or, without a graph,
-    launches the steps eagerly) and ev holds the per-launch event pairs (or [])."""
-    def make_events(external):
-        return [(torch.cuda.Event(enable_timing=True, external=external),
-                 torch.cuda.Event(enable_timing=True, external=external)) for _ in range(steps)] if events else []
+def capture_steps(torch, step, steps: int, stream):
+    """Capture `steps` launches on `stream` in one CUDA graph and replay it once untimed
+    (upload); returns its replay function, or None if capture fails (reported)."""
+    try:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            for _ in range(steps):
+                step()
+        graph.replay()
+        torch.cuda.synchronize()
+        return graph.replay
+    except Exception as e:                 # pragma: no cover - reported in the line
+        log("CUDA graph capture failed, timing eager launches:", repr(e))
+        return None
 
-    ev = make_events(use_graph)
 
-    def body():
-        for k in range(steps):
-            if flush_buf is not None:
-                flush_buf.zero_()
-            if ev:
-                ev[k][0].record()
-            step()
-            if ev:
-                ev[k][1].record()
-
-    if use_graph:
-        try:
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=stream):
-                body()
-            graph.replay()
-            torch.cuda.synchronize()
-            return graph.replay, ev
-        except Exception as e:                 # pragma: no cover - reported in the line
-            log("CUDA graph capture failed, timing eager launches:", repr(e))
-            ev = make_events(False)
-    return body, ev
+def evented_steps(torch, step, steps: int, flush_buf):
+    """Eager launches with a CUDA event pair around each (on the current stream), and an
+    L2 flush memset before each when flush_buf is given; returns the event pairs."""
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for k in range(steps):
+        if flush_buf is not None:
+            flush_buf.zero_()
+        ev[k][0].record()
+        step()
+        ev[k][1].record()
+    return ev
 
 
 def run_ours(args, rank, world, local_rank):
@@ -404,38 +408,67 @@ def run_ours(args, rank, world, local_rank):
     fbuf = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if flush else None
 
     # ---------------- device-resident timing (the headline `value`)
-    # The timed region replays one CUDA graph of the K steps.  Without a flush it holds only
-    # the K launches (value = K steps / its duration); a second graph with an external event
-    # pair around every launch, replayed right after, gives the per-launch durations (the
-    # roofline's launch time, p10/median/p90).  With a flush the timed graph is the evented
-    # one and value comes from the summed launches (the memsets are outside the events).
-    use_graph = not args.no_graph
+    # Timed region: one CUDA graph of the K launches (value = K steps / its duration,
+    # bracketed by barrier + synchronize).  Per-launch kernel durations (roofline launch
+    # time, p10/median/p90): K eager launches with an event pair around each, right after.
+    # With an L2 flush (small workloads) the timed region is those evented launches with a
+    # 2 x L2 memset before each, and value comes from the summed launch events.
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize(dev)
-        run_ev, ev = capture_steps(torch, step, args.steps, stream, fbuf, use_graph, events=True)
-        run_t = run_ev if flush else capture_steps(torch, step, args.steps, stream, None, use_graph, events=False)[0]
-        graph_used = use_graph and run_t is not None and getattr(run_t, "__self__", None) is not None
+        run_t = None if (flush or args.no_graph) else capture_steps(torch, step, args.steps, stream)
+        graph_used = run_t is not None
         if dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
+        ev = None
         with ClockSampler(torch, dev) as clk:
             g0.record()
-            run_t()
+            if run_t is not None:
+                run_t()
+            elif flush:
+                ev = evented_steps(torch, step, args.steps, fbuf)
+            else:
+                for _ in range(args.steps):
+                    step()
             g1.record()
             torch.cuda.synchronize(dev)
         if dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
-        if not flush:        # per-launch durations, right after the timed region
-            run_ev()
+        if ev is None:       # per-launch durations (distribution), after a short idle
+            time.sleep(0.5)  # let clock / power management return to its idle state
+            ev = evented_steps(torch, step, args.steps, None)
             torch.cuda.synchronize(dev)
+        # sustained: the timed graph replayed back to back for ~--sustained-seconds (power /
+        # clock management settles after ~0.1 s on this pool's B200s; the K-step timed region
+        # above is a burst), clocks sampled alongside; reported next to `value`, not instead
+        sustained = None
+        if run_t is not None and args.sustained_seconds > 0:
+            reps = max(1, int(np.ceil(args.sustained_seconds * 1e3 / max(1e-3, g0.elapsed_time(g1)))))
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            with ClockSampler(torch, dev) as sclk:
+                s0.record()
+                for _ in range(reps):
+                    run_t()
+                s1.record()
+                torch.cuda.synchronize(dev)
+            st_ms = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device=dev)
+            if dist:
+                dist.all_reduce(st_ms, op=dist.ReduceOp.MAX)
+            sustained = {"steps": reps * args.steps, "seconds": float(st_ms[0]) / 1e3,
+                         "ms_per_step": float(st_ms[0]) / (reps * args.steps), "clocks": sclk.summary()}
     launch_ms = np.array([a.elapsed_time(b) for a, b in ev])
     total_ms = float(launch_ms.sum()) if flush else g0.elapsed_time(g1)
-    t = torch.tensor([total_ms, float(launch_ms.mean()), float(np.median(launch_ms))], dtype=torch.float64,
-                     device=dev)
+    # roofline launch time: the timed region's time per step (it holds only the K decode
+    # launches; conservative by the ~1 us graph gaps), or the summed launches with a flush
+    step_launch_ms = total_ms / args.steps if not flush else float(launch_ms.mean())
+    t = torch.tensor([total_ms, step_launch_ms, float(np.median(launch_ms))], dtype=torch.float64, device=dev)
     n = torch.tensor([float(L.total_t), float(alg_bytes)], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -443,6 +476,9 @@ def run_ours(args, rank, world, local_rank):
     max_ms, max_launch_ms, max_median_ms = float(t[0]), float(t[1]), float(t[2])
     tri_all, bytes_all = float(n[0]), float(n[1])
     value = tri_all * args.steps / (max_ms * 1e-3) / 1e9
+    if sustained is not None:
+        sustained["value"] = tri_all / (sustained["ms_per_step"] * 1e-3) / 1e9
+        sustained["unit"] = UNIT
 
     cull_info = None
     if args.cull:
@@ -524,12 +560,15 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": int(alg_bytes), "launch_ms": max_launch_ms},
         "step_ms": {"p10": float(q[0]), "median": float(q[1]), "p90": float(q[2]), "mean": float(launch_ms.mean()),
-                    "max_rank_median": max_median_ms,
-                    "timing": (("timed: one CUDA graph of the K launches; per-launch: a second graph with external "
-                                "events around each launch, replayed right after" if not flush else
-                                "timed: one CUDA graph of the K launches + L2 flushes, external events around each "
-                                "launch") if graph_used else "eager launches, events around each launch")},
+                    "max_rank_median": max_median_ms, "roofline_launch_ms": max_launch_ms,
+                    "timing": ("timed: one CUDA graph of the K launches (roofline launch time = its time per "
+                               "step); per-launch distribution: K eager launches with events around each, after "
+                               "0.5 s idle" if graph_used else
+                               "timed: K eager launches with an L2 flush before each, events around each launch "
+                               "(value from the summed launches)" if flush else
+                               "timed: K eager launches; per-launch: K evented eager launches right after")},
         "hbm_gbs_aggregate": bytes_all * args.steps / (max_ms * 1e-3) / 1e9,
+        "sustained": sustained,
         "cpu_baseline": cpu,
         "parity": parity,
         "e2e": e2e,
@@ -562,6 +601,8 @@ def main():
     ap.add_argument("--instances", type=int, default=1000,
                     help="cfg4 instances: of the whole scene (strong) or per rank (weak)")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA graph")
+    ap.add_argument("--sustained-seconds", type=float, default=1.0,
+                    help="after timing, replay the timed graph for this long and report it as `sustained` (0: skip)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--e2e-chunks", type=int, default=32, help="mc_decode_host pipeline depth (0/1 = serial)")

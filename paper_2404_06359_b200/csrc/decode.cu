@@ -279,7 +279,10 @@ mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s, const ui
     // attribute mode: 0 aligned halfwords (every channel 16 bits, no VW), 1 bit reader, 2 VW
     bool b16 = true;
     for (uint32_t c = 0; c < L.n; ++c) b16 = b16 && L.bits[c] == 16;
-    const int am = (L.flags & 1u) ? 2 : (b16 ? 0 : 1);
+    bool uni = L.n > 0;
+    for (uint32_t c = 0; c < L.n; ++c) uni = uni && L.bits[c] == L.bits[0];
+    // 3: one width for every channel (compile-time unpack for the widths dispatch_am knows)
+    const int am = (L.flags & 1u) ? 2 : (b16 ? 0 : (uni && MC_UNIFORM_WIDTHS ? 3 : 1));
     if (lay == 0)   // generic kernel stages vertex words in smem
         P.vtx_stage_words = a->d_vertices ? ((L.v_max * L.n_out + 8u + 3u) & ~3u) : 0u;
     // group stride = 16 (mod 32) words: the two groups of a warp reading the same

@@ -2,7 +2,7 @@
 
     python scripts/ncu_summary.py gpurun_out/prof.ncu-rep <name> <workload> <units-per-launch>
 
-The JSON keeps, per workload, the DRAM bytes of one launch of the decode kernel
+MC_PROFILES_DIR overrides the output directory (profiles/).  The JSON keeps, per workload, the DRAM bytes of one launch of the decode kernel
 (`dram__bytes_read.sum + dram__bytes_write.sum`), which bench.py reports as
 roofline.traffic.
 """
@@ -53,10 +53,11 @@ def main():
         lines.append(f"DRAM GB/s under ncu (cold, serialised): {dram / t / 1e9:.1f}")
     if "smsp__inst_executed.sum" in res:
         lines.append(f"warp-instructions per unit: {res['smsp__inst_executed.sum'] / units:.1f}")
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    with open(os.path.join(ROOT, "profiles", f"{name}.txt"), "w") as f:
+    outdir = os.environ.get("MC_PROFILES_DIR", os.path.join(ROOT, "profiles"))
+    os.makedirs(outdir, exist_ok=True)
+    with open(os.path.join(outdir, f"{name}.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    js = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    js = os.path.join(outdir, "ncu_summary.json")
     data = json.load(open(js)) if os.path.exists(js) else {}
     data[workload] = {"dram_bytes_per_launch": dram, "report": name, "kernel_time_s_ncu": t,
                       "warp_instructions_per_meshlet": res.get("smsp__inst_executed.sum", 0) / units,

@@ -22,6 +22,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 SEM_GENERIC, SEM_POSITION, SEM_NORMAL, SEM_TEXCOORD, SEM_OCT = 0, 1, 2, 3, 4
@@ -242,12 +244,20 @@ def building(k: int, seed: int, bits: int = 16) -> Mesh:
 
 
 def city(num_instances: int = 1000, num_prototypes: int = 16, k: int = 91, seed: int = 0,
-         bits: int = 16) -> InstancedScene:
-    """cfg4: instanced city — ``num_prototypes`` seeded buildings of 12*k^2 tris
-    (k=91 -> 99,372) placed ``num_instances`` times on a jittered 2-D grid
-    (1000 x 99,372 ≈ 99.4M tris)."""
+         bits: int = 16, k_jitter: int = 0) -> InstancedScene:
+    """cfg4: instanced city — ``num_prototypes`` seeded buildings of 12*k_p^2 tris placed
+    ``num_instances`` times on a jittered 2-D grid.  k_p = k (k=91 -> 99,372 tris) or, with
+    k_jitter > 0, a seeded k_p in [k - k_jitter, k + k_jitter] per building (different
+    subdivision, so different meshlet partitions and strips; mean ≈ 12 k^2 tris)."""
     rng = np.random.default_rng(seed)
-    protos = [building(k, seed * 1000 + p, bits) for p in range(num_prototypes)]
+    ks = [k] * num_prototypes if k_jitter <= 0 else \
+        [int(x) for x in np.random.default_rng(seed + 77).integers(k - k_jitter, k + k_jitter + 1, num_prototypes)]
+    if num_prototypes > 8:   # independent seeded meshes: build them on host threads
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(min(32, os.cpu_count() or 1)) as ex:
+            protos = list(ex.map(lambda p: building(ks[p], seed * 1000 + p, bits), range(num_prototypes)))
+    else:
+        protos = [building(ks[p], seed * 1000 + p, bits) for p in range(num_prototypes)]
     side = int(np.ceil(np.sqrt(num_instances)))
     gi = np.arange(num_instances)
     gx, gy = gi % side, gi // side
@@ -257,7 +267,7 @@ def city(num_instances: int = 1000, num_prototypes: int = 16, k: int = 91, seed:
     off[:, 1] = gy * 32.0 + jitter[:, 1]
     proto = rng.integers(0, num_prototypes, size=num_instances).astype(np.uint32)
     return InstancedScene(protos, proto, off, f"city{num_instances}",
-                          {"k": k, "num_prototypes": num_prototypes, "seed": seed})
+                          {"k": k, "k_jitter": k_jitter, "num_prototypes": num_prototypes, "seed": seed})
 
 
 def random_patch(seed: int, nx: int = 12, ny: int = 9, drop: float = 0.15, n_ch: int = 5,

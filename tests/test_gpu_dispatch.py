@@ -3,8 +3,9 @@
 decode.cu picks a kernel per launch: the static-stride short-launch kernel (u32 output,
 compile-time halfword layout, fewer than MC_STATIC_BELOW records per group of a full
 grid: < 56,832 records on 148 SMs), the dynamic-claim kernels above that (the u8x4-only
-build for the strip codecs' u8x4 output), 16-lane groups with K = 1 flag word for T~ <= 32,
-K = 4 for T~ <= 128, 32-lane groups for T~ > 128, the bit reader (widths != 16) and the
+build for the strip codecs' u8x4 output), 8-lane groups with K = 1 flag word for T~ <= 32,
+16-lane groups with K = 2 for T~ <= 64 and K = 4 for T~ <= 128, 32-lane groups for
+T~ > 128, the bit reader (widths != 16) and the
 per-meshlet-width reader (VW).  Each case below builds a blob of the size that selects the
 kernel (instanced small prototypes: >= 60,000 records for the dynamic kernels) and compares
 the NON-stats decode (the timed path) element by element with the oracle's sequential
@@ -91,18 +92,27 @@ def test_static_stride_kernel(mc, orc, codec, layout):
 
 
 @pytest.mark.parametrize("fmt", ["u32", "u8x4"])
-@pytest.mark.parametrize("limits", [(32, 32), (128, 256), (256, 256)])
+@pytest.mark.parametrize("limits", [(32, 32), (64, 64), (128, 256), (256, 256)])
 @pytest.mark.parametrize("codec", [1, 2])
 def test_group_shapes(mc, orc, codec, limits, fmt):
-    """T~ <= 32 (16-lane groups, one flag word per step) and T~ > 128 (32-lane groups)."""
+    """T~ <= 32 (8-lane groups, one flag word per step), T~ <= 64 (16-lane groups, two flag
+    words per step) and T~ > 128 (32-lane groups)."""
     _check(mc, orc, _instanced(mc, "n7oct", codec, limits, 60000), fmt)
 
 
-@pytest.mark.parametrize("bits", [8, 12, 24])
-@pytest.mark.parametrize("layout", ["n3", "n8"])
-def test_bit_reader_kernels(mc, orc, layout, bits):
-    """Widths != 16: the funnel-shift bit reader at the dynamic launch size."""
-    _check(mc, orc, _instanced(mc, layout, 2, (64, 126), 60000, bits=bits), "u32")
+@pytest.mark.parametrize("layout,bits", [("n3", 8), ("n3", 12), ("n3", 24), ("n8", 8), ("n8", 10), ("n8", 12),
+                                         ("n8", 20), ("n8", 24)])
+@pytest.mark.parametrize("limits", [(64, 126), (32, 32), (128, 256)])
+def test_bit_reader_kernels(mc, orc, layout, bits, limits):
+    """Widths != 16 at the dynamic launch size: n = 8 with one width for every channel takes
+    the compile-time unpack (units of word-aligned vertices), n = 3 the run-time funnel-shift
+    bit reader."""
+    _check(mc, orc, _instanced(mc, layout, 2, limits, 60000, bits=bits), "u32")
+
+
+@pytest.mark.parametrize("codec", [1, 3])
+def test_uniform_width_other_codecs(mc, orc, codec):
+    _check(mc, orc, _instanced(mc, "n8", codec, (64, 126), 60000, bits=10), "u8x4")
 
 
 @pytest.mark.parametrize("fmt", ["u32", "u8x4"])
