@@ -152,12 +152,26 @@ def config_dict(args, L, meta, world: int, alg_bytes: int, flush: bool) -> dict:
             **meta}
 
 
+def allreduce(dist, t, op=None):
+    """All-reduce a tensor in place (NCCL on the GPU; gloo on a host copy when ranks share
+    one GPU — the functional multi-rank test on a 1-GPU box).  No-op without dist."""
+    if dist is None:
+        return t
+    op = dist.ReduceOp.SUM if op is None else op
+    if dist.get_backend() == "gloo" and t.is_cuda:
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op)
+    return t
+
+
 def allreduce_u64_sum(values, dist, device):
     """All-reduce u64 checksums (FORMAT.md §6): int64 sum wraps mod 2^64 exactly like u64."""
     import torch
     t = torch.tensor(np.array(values, dtype=np.uint64).view(np.int64), device=device)
-    if dist is not None:
-        dist.all_reduce(t)
+    allreduce(dist, t)
     return [int(x) for x in t.cpu().numpy().view(np.uint64)]
 
 
@@ -295,12 +309,17 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload: str, index_format: str, scaling: str, world: int):
-    """DRAM bytes per launch from the committed ncu --set full capture of this build
-    (profiles/ncu_summary.json, scripts/ncu_summary.py), for the same launch shape."""
+def ncu_traffic(args, world: int):
+    """DRAM bytes per launch from the committed ncu --set full capture of the same launch
+    shape (profiles/ncu_summary.json, written by scripts/ncu_summary.py), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    key = workload + ("" if index_format == "u32" else "_" + index_format) + \
-        ("" if world == 1 or scaling == "weak" else f"_strong{world}")
+    key = args.workload
+    if args.workload == "cfg4_city":
+        per_rank = args.instances / world if args.scaling == "strong" else args.instances
+        if per_rank != 1000:
+            key += f"_strong{int(round(1000 / per_rank))}" if 1000 % per_rank == 0 else "_unprofiled"
+    key += ("_" + args.index_format if args.index_format != "u32" else "") + ("_vw" if args.variable_widths else "") + \
+        ("_cull" if args.cull else "") + ("" if args.codec == 2 else f"_codec{args.codec}")
     try:
         e = json.load(open(p))[key]
         return e["dram_bytes_per_launch"], e.get("report")
@@ -318,7 +337,7 @@ def run_reference(args, rank, world):
     oracle.build()
     import paper_2404_06359_b200 as mc
     blob, meta = build_blob(mc, args.workload, 0, world, args.codec, args.instances, vw=args.variable_widths,
-                            scaling=args.scaling)
+                            scaling=args.scaling, protos_k=(args.prototypes, 91))
     data = np.array(blob.bytes)
     L = blob.layout
     alg = algorithmic_bytes(L, args.index_format)
@@ -377,15 +396,22 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import paper_2404_06359_b200 as mc
     mc.lib()
-    dev = torch.device("cuda", local_rank)
+    # one rank per GPU; if there are fewer GPUs than local ranks (a functional multi-rank
+    # run on a 1-GPU box) ranks share devices and the collectives use gloo on host copies
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local_rank % ndev)
     torch.cuda.set_device(dev)
-    dist = None
+    dist, backend = None, None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = "nccl" if ndev >= int(os.environ.get("LOCAL_WORLD_SIZE", world)) else "gloo"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     t0 = time.time()
     blob, meta = build_blob(mc, args.workload, rank, world, args.codec, args.instances, vw=args.variable_widths,
-                            cull=args.cull, scaling=args.scaling)
+                            cull=args.cull, scaling=args.scaling, protos_k=(args.prototypes, 91))
     L = blob.layout
     log(f"[rank {rank}] scene built in {time.time() - t0:.1f}s: {L.num_meshlets} meshlets, "
         f"T={L.total_t} T'={L.total_tp} V={L.total_v}, {L.total_bytes / 1e6:.1f} MB")
@@ -460,7 +486,7 @@ def run_ours(args, rank, world, local_rank):
                 torch.cuda.synchronize(dev)
             st_ms = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device=dev)
             if dist:
-                dist.all_reduce(st_ms, op=dist.ReduceOp.MAX)
+                allreduce(dist, st_ms, dist.ReduceOp.MAX)
             sustained = {"steps": reps * args.steps, "seconds": float(st_ms[0]) / 1e3,
                          "ms_per_step": float(st_ms[0]) / (reps * args.steps), "clocks": sclk.summary()}
     launch_ms = np.array([a.elapsed_time(b) for a, b in ev])
@@ -471,8 +497,8 @@ def run_ours(args, rank, world, local_rank):
     t = torch.tensor([total_ms, step_launch_ms, float(np.median(launch_ms))], dtype=torch.float64, device=dev)
     n = torch.tensor([float(L.total_t), float(alg_bytes)], dtype=torch.float64, device=dev)
     if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        allreduce(dist, t, dist.ReduceOp.MAX)
+        allreduce(dist, n, dist.ReduceOp.SUM)
     max_ms, max_launch_ms, max_median_ms = float(t[0]), float(t[1]), float(t[2])
     tri_all, bytes_all = float(n[0]), float(n[1])
     value = tri_all * args.steps / (max_ms * 1e-3) / 1e9
@@ -496,7 +522,7 @@ def run_ours(args, rank, world, local_rank):
     checksum = allreduce_u64_sum([st["checksum_indices"], st["checksum_vertices"]], dist, dev)
     errs = torch.tensor([st["error_bits"]], dtype=torch.int64, device=dev)
     if dist:
-        dist.all_reduce(errs)
+        allreduce(dist, errs)
 
     # ---------------- end to end through the C ABI with pinned HOST buffers
     e2e = None
@@ -521,7 +547,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize(dev)
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if dist:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            allreduce(dist, et, dist.ReduceOp.MAX)
         e2e = {"value": tri_all * ke / (float(et[0]) * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(data.nbytes), "d2h_bytes_per_step": int(4 * idx_words + 4 * L.n_out * L.total_v),
                "steps": ke, "chunks": args.e2e_chunks,
@@ -534,7 +560,7 @@ def run_ours(args, rank, world, local_rank):
         return
     peak, peak_src = peak_hbm()
     achieved = alg_bytes / (max_launch_ms * 1e-3) / 1e9
-    traffic, traffic_src = ncu_traffic(args.workload, args.index_format, args.scaling, world)
+    traffic, traffic_src = ncu_traffic(args, world)
     cpu, parity = None, None
     if not args.no_cpu_baseline and world == 1:
         import oracle
@@ -553,6 +579,7 @@ def run_ours(args, rank, world, local_rank):
     q = np.percentile(launch_ms, [10, 50, 90])
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "dist_backend": backend, "devices_shared": bool(world > ndev),
         "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "u32/fp32", "data": "synthetic",
         "config": config_dict(args, L, meta, world, alg_bytes, flush),
@@ -600,6 +627,7 @@ def main():
                     help="u32: 3 global indices per triangle (default); u8x4: one local u8x4 word")
     ap.add_argument("--instances", type=int, default=1000,
                     help="cfg4 instances: of the whole scene (strong) or per rank (weak)")
+    ap.add_argument("--prototypes", type=int, default=CITY_PROTOTYPES, help="cfg4 seeded buildings")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA graph")
     ap.add_argument("--sustained-seconds", type=float, default=1.0,
                     help="after timing, replay the timed graph for this long and report it as `sustained` (0: skip)")

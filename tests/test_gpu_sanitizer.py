@@ -26,6 +26,8 @@ def test_sanitizer_clean(tool):
     # racecheck counts its (TMA false-positive) warnings in the exit code: its hazards are
     # parsed below instead
     cmd = [SAN, "--tool", tool, "--print-limit", "20"] + ([] if tool == "racecheck" else ["--error-exitcode", "99"])
+    if tool in ("racecheck", "synccheck"):   # 8-lane groups: 32 groups x 2 mbarriers per CTA
+        cmd += ["--num-cuda-barriers", "128"]
     if tool == "memcheck":
         cmd += ["--leak-check", "no"]
     args = [sys.executable, os.path.join(ROOT, "tests", "sanitize_decode.py")] + (["--big"] if tool == "memcheck" else [])
