@@ -420,9 +420,9 @@ def run_ours(args, rank, world, local_rank):
     view_dir = np.array([1.0, 2.0, -3.0], np.float64)
     view_dir = (view_dir / np.linalg.norm(view_dir)).astype(np.float32)
     stream = torch.cuda.Stream(dev)
-    if args.cull:   # FORMAT.md §7: one step = cull + scan + emit + decode of the visible records
+    if args.cull:   # FORMAT.md §7: one step = one-pass cull scan + decode of the visible records
         step = lambda: db.decode_culled(view_dir)
-        launches_per_step = 4
+        launches_per_step = 2
     else:
         step = lambda: db.decode()
         launches_per_step = 1

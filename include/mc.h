@@ -267,7 +267,11 @@ mc_status mc_decode_stats(const mc_decode_args *args, mc_stats *d_stats, void *s
  * mc_decode_meshlets (the visible part is a prefix of them).  d_counts (device,
  * uint32_t[4]) receives {visible records, Σ V, Σ T', Σ T (real)}; d_stats (device or
  * NULL) accumulates mc_stats over the visible records.  d_scratch: device, 16-B aligned,
- * >= mc_decode_culled_scratch_bytes(layout).  Asynchronous: four kernels on `stream`.
+ * >= mc_decode_culled_scratch_bytes(layout), caller-owned, zero-filled once before its
+ * first use: every completed call leaves its look-back flags and tile tickets zero again
+ * (two calls in flight at the same time must not share one).  Asynchronous: two kernels
+ * on `stream` — a one-pass cone test + decoupled look-back scan that lists the visible
+ * records with their compacted output bases, then the decode kernel over that list.
  * Errors: MC_ERR_FORMAT (blob without cull table), MC_ERR_ARG, MC_ERR_LIMITS, MC_ERR_CUDA. */
 size_t mc_decode_culled_scratch_bytes(const mc_layout *layout);
 mc_status mc_decode_culled(const mc_decode_args *args, const float *view_dir, void *d_scratch, size_t scratch_bytes,

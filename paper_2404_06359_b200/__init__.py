@@ -413,7 +413,8 @@ class DeviceBlob:
         L = self.layout
         if getattr(self, "cull_scratch", None) is None:
             nb = lib().mc_decode_culled_scratch_bytes(ctypes.byref(L))
-            self.cull_scratch = torch.empty((nb + 15) // 16 * 16, dtype=torch.uint8, device=self.d_blob.device)
+            # zero once: every completed culled decode leaves its look-back flags zero (mc.h)
+            self.cull_scratch = torch.zeros((nb + 15) // 16 * 16, dtype=torch.uint8, device=self.d_blob.device)
             self.cull_counts = torch.zeros(4, dtype=torch.int32, device=self.d_blob.device)
         _check_sizes(L, self.d_blob, self.indices, self.vertices, self.quantized, flags | self.index_flags)
         a = mc_decode_args(ctypes.pointer(L), self.d_blob.data_ptr(), 0, L.num_meshlets, self.indices.data_ptr(),

@@ -72,9 +72,9 @@ __global__ void stats_reset_kernel(mc_stats* s) {
 
 // ------------------------------------------------------------------ cone culling (FORMAT.md §1.5, §7)
 // The paper's amplification-shader pass: per record, the binary32 cone test
-// fmaf(az,dz, fmaf(ay,dy, ax*dx)) > cutoff, then a three-kernel reduce / scan / emit that
-// lists the visible records in record order with their compacted output bases.  The
-// decode kernel then walks that list (Params::list).
+// fmaf(az,dz, fmaf(ay,dy, ax*dx)) > cutoff and a one-pass decoupled look-back scan
+// (cull_scan_kernel) that lists the visible records in record order with their compacted
+// output bases.  The decode kernel then walks that list (Params::list): two launches.
 constexpr int kCullThreads = 256, kCullPerThread = 8, kCullTile = kCullThreads * kCullPerThread;
 
 struct CullParams {
@@ -84,8 +84,10 @@ struct CullParams {
     uint64_t rec_section_bytes;
     uint32_t M, vmax, tmax, max_rec;
     float dx, dy, dz;
-    uint4* tile_sum;      // [tiles] {records, V, T', T}
-    uint4* tile_off;      // [tiles] exclusive prefix of tile_sum
+    uint4* tile_agg;      // [tiles] tile totals {records, V, T', T} (look-back status 1)
+    uint4* tile_inc;      // [tiles] inclusive prefix through the tile (look-back status 2)
+    uint32_t* tile_flag;  // [tiles] 0 = not yet, 1 = aggregate published, 2 = inclusive published
+    uint32_t* ctr;        // [4]: tile ticket, CTAs done (zero at launch, left zero)
     uint4* list;          // [M] {m, VB, TB, 0}
     uint32_t* counts;     // [4] totals {records, V, T', T}
     uint32_t tiles;
@@ -126,40 +128,29 @@ __device__ __forceinline__ uint4 block_scan4(uint4 v, uint4* sh /* [kCullThreads
     return add4(v, pre);
 }
 
-__global__ void __launch_bounds__(kCullThreads) cull_reduce_kernel(const CullParams C) {
-    __shared__ uint4 sh[kCullThreads / 32];
-    const uint32_t base = blockIdx.x * kCullTile + threadIdx.x * kCullPerThread;
-    uint4 acc = make_uint4(0, 0, 0, 0);
-    for (int i = 0; i < kCullPerThread; ++i) acc = add4(acc, cull_one(C, base + i));
-    const uint4 inc = block_scan4(acc, sh);
-    if (threadIdx.x == kCullThreads - 1) C.tile_sum[blockIdx.x] = inc;
+// One pass (a decoupled look-back scan, no host round trip, one launch): each CTA takes
+// the next tile of kCullTile records by ticket, tests its records, publishes the tile
+// total, looks back over the predecessors' published totals / inclusive prefixes for its
+// exclusive prefix, publishes its inclusive prefix and writes its visible records' list
+// entries {m, VB, TB} in record order.  The last tile writes the totals.  The last CTA to
+// finish clears the flags and tickets, so the scratch is zero again for the next call.
+__device__ __forceinline__ uint4 ld_volatile4(const uint4* p) {
+    const volatile uint32_t* q = reinterpret_cast<const volatile uint32_t*>(p);
+    return make_uint4(q[0], q[1], q[2], q[3]);
+}
+__device__ __forceinline__ void st_volatile4(uint4* p, uint4 v) {
+    volatile uint32_t* q = reinterpret_cast<volatile uint32_t*>(p);
+    q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
 }
 
-__global__ void __launch_bounds__(kCullThreads) cull_scan_tiles_kernel(const CullParams C) {
+__global__ void __launch_bounds__(kCullThreads) cull_scan_kernel(const CullParams C) {
     __shared__ uint4 sh[kCullThreads / 32];
-    __shared__ uint4 chunk_total;
-    uint4 carry = make_uint4(0, 0, 0, 0);
-    for (uint32_t t0 = 0; t0 < C.tiles; t0 += kCullThreads) {
-        const uint32_t t = t0 + threadIdx.x;
-        const uint4 v = t < C.tiles ? C.tile_sum[t] : make_uint4(0, 0, 0, 0);
-        const uint4 inc = block_scan4(v, sh);
-        if (t < C.tiles) C.tile_off[t] = add4(carry, make_uint4(inc.x - v.x, inc.y - v.y, inc.z - v.z, inc.w - v.w));
-        if (threadIdx.x == kCullThreads - 1) chunk_total = inc;
-        __syncthreads();
-        carry = add4(carry, chunk_total);
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        C.counts[0] = carry.x;
-        C.counts[1] = carry.y;
-        C.counts[2] = carry.z;
-        C.counts[3] = carry.w;
-    }
-}
-
-__global__ void __launch_bounds__(kCullThreads) cull_emit_kernel(const CullParams C) {
-    __shared__ uint4 sh[kCullThreads / 32];
-    const uint32_t base = blockIdx.x * kCullTile + threadIdx.x * kCullPerThread;
+    __shared__ uint32_t s_tile, s_last;
+    __shared__ uint4 s_excl, s_agg;
+    if (threadIdx.x == 0) s_tile = atomicAdd(C.ctr, 1u);     // tiles in CTA start order
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t base = tile * kCullTile + threadIdx.x * kCullPerThread;
     uint4 v[kCullPerThread];
     uint4 acc = make_uint4(0, 0, 0, 0);
 #pragma unroll
@@ -168,11 +159,63 @@ __global__ void __launch_bounds__(kCullThreads) cull_emit_kernel(const CullParam
         acc = add4(acc, v[i]);
     }
     const uint4 inc = block_scan4(acc, sh);
-    uint4 run = add4(C.tile_off[blockIdx.x], make_uint4(inc.x - acc.x, inc.y - acc.y, inc.z - acc.z, inc.w - acc.w));
+    if (threadIdx.x == kCullThreads - 1) s_agg = inc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint4 agg = s_agg;
+        uint4 excl = make_uint4(0, 0, 0, 0);
+        if (tile == 0) {
+            st_volatile4(C.tile_inc, agg);
+            __threadfence();
+            atomicExch(C.tile_flag, 2u);
+        } else {
+            st_volatile4(C.tile_agg + tile, agg);
+            __threadfence();
+            atomicExch(C.tile_flag + tile, 1u);
+            for (int j = (int)tile - 1; j >= 0; --j) {
+                uint32_t f;
+                while ((f = atomicAdd(C.tile_flag + j, 0u)) == 0u) {
+                }
+                __threadfence();
+                if (f == 2u) {
+                    excl = add4(excl, ld_volatile4(C.tile_inc + j));
+                    break;
+                }
+                excl = add4(excl, ld_volatile4(C.tile_agg + j));
+            }
+            st_volatile4(C.tile_inc + tile, add4(excl, agg));
+            __threadfence();
+            atomicExch(C.tile_flag + tile, 2u);
+        }
+        if (tile == C.tiles - 1) {
+            const uint4 tot = add4(excl, agg);
+            C.counts[0] = tot.x;
+            C.counts[1] = tot.y;
+            C.counts[2] = tot.z;
+            C.counts[3] = tot.w;
+        }
+        s_excl = excl;
+    }
+    __syncthreads();
+    uint4 run = add4(s_excl, make_uint4(inc.x - acc.x, inc.y - acc.y, inc.z - acc.z, inc.w - acc.w));
 #pragma unroll
     for (int i = 0; i < kCullPerThread; ++i) {
         if (v[i].x) C.list[run.x] = make_uint4(base + i, run.y, run.z, 0u);
         run = add4(run, v[i]);
+    }
+    // leave the scratch zeroed: the last CTA clears flags and tickets
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(C.ctr + 1, 1u) == C.tiles - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (s_last) {
+        for (uint32_t t = threadIdx.x; t < C.tiles; t += kCullThreads) C.tile_flag[t] = 0u;
+        if (threadIdx.x == 0) {
+            C.ctr[0] = 0u;
+            C.ctr[1] = 0u;
+        }
     }
 }
 
@@ -378,7 +421,8 @@ mc_status mc_decode_stats(const mc_decode_args* args, mc_stats* d_stats, void* s
 size_t mc_decode_culled_scratch_bytes(const mc_layout* L) {
     if (!L) return 0;
     const uint64_t tiles = (uint64_t(L->num_meshlets) + kCullTile - 1) / kCullTile;
-    return size_t(16ull * L->num_meshlets + 32ull * tiles + 16ull);
+    // list [M] uint4 | tile_agg [tiles] uint4 | tile_inc [tiles] uint4 | tile_flag [tiles] u32 | ctr [4] u32
+    return size_t(16ull * L->num_meshlets + 32ull * tiles + ((4ull * tiles + 15) & ~15ull) + 16ull);
 }
 
 mc_status mc_decode_culled(const mc_decode_args* a, const float* view_dir, void* d_scratch, size_t scratch_bytes,
@@ -409,12 +453,12 @@ mc_status mc_decode_culled(const mc_decode_args* a, const float* view_dir, void*
     C.dz = view_dir[2];
     C.tiles = (M + kCullTile - 1) / kCullTile;
     C.list = static_cast<uint4*>(d_scratch);
-    C.tile_sum = C.list + M;
-    C.tile_off = C.tile_sum + C.tiles;
+    C.tile_agg = C.list + M;
+    C.tile_inc = C.tile_agg + C.tiles;
+    C.tile_flag = reinterpret_cast<uint32_t*>(C.tile_inc + C.tiles);
+    C.ctr = C.tile_flag + ((C.tiles + 3u) & ~3u);
     C.counts = d_counts;
-    cull_reduce_kernel<<<C.tiles, kCullThreads, 0, s>>>(C);
-    cull_scan_tiles_kernel<<<1, kCullThreads, 0, s>>>(C);
-    cull_emit_kernel<<<C.tiles, kCullThreads, 0, s>>>(C);
+    cull_scan_kernel<<<C.tiles, kCullThreads, 0, s>>>(C);
     if (cudaGetLastError() != cudaSuccess) return MC_ERR_CUDA;
     return launch(a, d_stats, s, C.list, d_counts);
 }
