@@ -545,3 +545,17 @@ def test_checksum_additivity(orc):
     full = orc.checksum(w, 0)
     parts = (orc.checksum(w[:313], 0) + orc.checksum(w[313:], 313)) % 2**64
     assert full == parts
+
+
+def test_checksum_splitmix64_vectors(orc):
+    """FORMAT.md §6's mix64 is the SplitMix64 finaliser; the published
+    SplitMix64 sequence for seed 0 is mix64(i * 0x9e3779b97f4a7c15) for i = 1, 2, 3:
+    0xe220a8397b1dcdaf, 0x6e789e6aa1b965f4, 0x06c45d188009454f.  A one-word buffer at word
+    index k holding w contributes mix64(k << 32 | w), so choosing (k, w) as the halves of
+    i * golden must reproduce those published values."""
+    golden = 0x9E3779B97F4A7C15
+    want = [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F]
+    for i, v in enumerate(want, start=1):
+        z = (golden * i) % 2**64
+        k, w = z >> 32, z & 0xFFFFFFFF
+        assert orc.checksum(np.array([w], np.uint32), k) == v
