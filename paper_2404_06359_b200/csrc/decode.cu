@@ -260,6 +260,7 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     P.hdr_words = ((16u + 4u * L.n + (P.vw ? L.n : 0u) + 15u) & ~15u) / 4u;
     P.buf_words = L.max_record_bytes / 4u + 4u;
     P.vtx_stage_words = 0;
+    P.idx_stage_words = 0;
     P.idx = a->d_indices;
     P.fout = a->d_vertices;
     P.qout = a->d_quantized;
@@ -330,7 +331,8 @@ mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s, const ui
         P.vtx_stage_words = a->d_vertices ? ((L.v_max * L.n_out + 8u + 3u) & ~3u) : 0u;
     // group stride = 16 (mod 32) words: the two groups of a warp reading the same
     // record offset hit different banks
-    P.grp_words = 2 * P.buf_words + P.vtx_stage_words + kMiscWords;
+    P.idx_stage_words = MC_BULK_IDX ? ((((P.u8x4 ? 1u : 3u) * L.t_max + 4u) + 3u) & ~3u) : 0u;
+    P.grp_words = 2 * P.buf_words + P.vtx_stage_words + P.idx_stage_words + kMiscWords;
     if (MC_BANK_PAD) P.grp_words += (48u - (P.grp_words & 31u)) & 31u;
     smem = 4u * (size_t)P.grp_words;
     return dispatch_codec(L.codec, st != nullptr, lay, am, P, smem, s);

@@ -8,7 +8,8 @@ grid width b in {8, 10, 12, 16, 20, 24} (all 8 channels: pos3 + nrm3 + uv2, SURV
 encode a seeded displaced cube-sphere (k = 300, 1.08M triangles) with the product encoder,
 instance it ``--instances`` times (distinct bytes in HBM, each instance its own grid), and
 time the decode kernel with CUDA events around each launch on its stream (3 warm-ups,
-``--steps`` timed; the per-step time including host launch gaps is reported beside it).
+``--steps`` timed after ``--idle`` seconds idle, NVML SM clock sampled during the timing; the
+per-step time including host launch gaps is reported beside it).
 Reports compressed bits per real triangle (whole blob: header + directory + records),
 record-only bits/tri, decode Gtri/s and algorithmic GB/s, and checks error_bits == 0.
 
@@ -26,6 +27,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import bench  # noqa: E402  (ClockSampler)
 import synth  # noqa: E402
 
 SIZES = [(32, 32), (64, 64), (64, 126), (128, 128), (128, 256), (256, 256)]
@@ -42,6 +44,7 @@ def main():
     ap.add_argument("--label", default="")
     ap.add_argument("--sizes", default="", help="subset, e.g. 128x256,256x256")
     ap.add_argument("--bits", default="", help="subset, e.g. 16,24")
+    ap.add_argument("--idle", type=float, default=1.0, help="seconds idle before each point's timing")
     args = ap.parse_args()
     import torch
     import paper_2404_06359_b200 as mc
@@ -68,13 +71,15 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
             torch.cuda.synchronize(dev)
-            e0.record(stream)
-            for k in range(args.steps):
-                ev[k][0].record(stream)
-                db.decode(stream=stream)
-                ev[k][1].record(stream)
-            e1.record(stream)
-            torch.cuda.synchronize(dev)
+            time.sleep(args.idle)   # every point starts from the same (idle) clock / power state
+            with bench.ClockSampler(torch, dev) as clk:
+                e0.record(stream)
+                for k in range(args.steps):
+                    ev[k][0].record(stream)
+                    db.decode(stream=stream)
+                    ev[k][1].record(stream)
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
             ms_total = e0.elapsed_time(e1) / args.steps
             ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))   # kernel time per launch
             alg = db.algorithmic_bytes()
@@ -86,7 +91,8 @@ def main():
                     "bits_per_tri": 8.0 * L.total_bytes / L.total_t, "record_bits_per_tri": 8.0 * rec_bytes / L.total_t,
                     "max_record_bytes": int(L.max_record_bytes),
                     "ms": ms, "ms_per_step_incl_launch_gaps": ms_total, "gtri_s": L.total_t / (ms * 1e-3) / 1e9, "alg_gb_s": alg / (ms * 1e-3) / 1e9,
-                    "alg_bytes": int(alg), "error_bits": int(st["error_bits"]), "wall_s": round(time.time() - t0, 2)}
+                    "alg_bytes": int(alg), "error_bits": int(st["error_bits"]), "wall_s": round(time.time() - t0, 2),
+                    "clocks": clk.summary()}
             print(json.dumps(line), flush=True)
             out.write(json.dumps(line) + "\n")
             del db
