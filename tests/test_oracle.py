@@ -188,18 +188,20 @@ def _adjacency(tris):
     return adj
 
 
-@pytest.mark.parametrize("mesh_id", range(4))
+@pytest.mark.parametrize("mesh_id", range(7))
 def test_bruteforce_path_covers_roundtrip(orc, mesh_id):
-    """Every path cover of tiny patches (<=5 triangles), encoded by an independent Python
-    encoder, decodes (GTS and Reuse) to the source triangles with winding preserved."""
+    """Every path cover (all path orders and directions) of tiny patches of 4-6 triangles
+    (SURVEY §8(c) "meshlets of <= 6 triangles"), encoded by an independent Python encoder,
+    decodes (GTS and Reuse) to the source triangles with winding preserved."""
     grid = synth.quad_grid(3, 2).indices
-    picks = [[0, 1, 2, 3], [0, 1, 2, 3, 4], [1, 2, 3, 4, 5], [2, 3, 6, 7, 8]][mesh_id]
+    picks = [[0, 1, 2, 3], [0, 1, 2, 3, 4], [1, 2, 3, 4, 5], [2, 3, 6, 7, 8],
+             [0, 1, 2, 3, 4, 5], [2, 3, 4, 5, 6, 7], [0, 1, 2, 3, 6, 7]][mesh_id]
     tris = [tuple(int(v) for v in grid[p]) for p in picks]
     adj = _adjacency(tris)
     covers = list(_path_covers(tris, adj))
-    assert len(covers) > 3
+    assert 3 < len(covers) <= 4000          # every cover is checked
     gts, reu, srcs = [], [], []
-    for cov in covers[:4000]:
+    for cov in covers:
         V, flags, N, src = py_strip_encode(tris, cov)
         gts.append(gts_meshlet(V, flags, N[3:]))
         inc, reuse = reuse_fields(N)
