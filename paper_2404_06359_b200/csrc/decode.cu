@@ -329,6 +329,8 @@ mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s, const ui
     const int am = (L.flags & 1u) ? 2 : (b16 ? 0 : (uni && MC_UNIFORM_WIDTHS ? 3 : 1));
     if (lay == 0)   // generic kernel stages vertex words in smem
         P.vtx_stage_words = a->d_vertices ? ((L.v_max * L.n_out + 8u + 3u) & ~3u) : 0u;
+    else if (MC_BULK_VTX && (L.n_out % 4u) == 0u)   // compile-time layouts with bulk vertex stores
+        P.vtx_stage_words = a->d_vertices ? ((L.v_max * L.n_out + 3u) & ~3u) : 0u;
     // group stride = 16 (mod 32) words: the two groups of a warp reading the same
     // record offset hit different banks
     P.idx_stage_words = MC_BULK_IDX ? ((((P.u8x4 ? 1u : 3u) * L.t_max + 4u) + 3u) & ~3u) : 0u;
