@@ -1,45 +1,36 @@
-// decode.cu — the hot path of libmc: per-meshlet decompression on sm_100a (B200).
+// decode.cu — host side of the libmc decode path (sm_100a, B200): argument checks, launch
+// planning, cone culling, the pipelined host decode and the C ABI entry points.  The kernel
+// family itself is decode_kernel.cuh, instantiated per codec x stats in decode_inst.cu.
 //
-// Paper: arXiv 2404.06359 §4.2–4.4.  A GROUP of G lanes decodes one meshlet record
-// (FORMAT.md) at a time and loops over records with a grid stride.  G = 16 by default:
-// each half-warp is an independent group with its own staging buffers, mbarriers and
-// lane mask, so the per-meshlet uniform work (header, validation, flag-word scans,
-// staging) is shared by two meshlets per warp instruction:
+// Paper: arXiv 2404.06359 §4.2–4.4.  A GROUP of G lanes (8, 16 or 32 by meshlet size)
+// decodes one meshlet record (FORMAT.md) at a time; groups claim records in global order
+// from interleaved device counters.  Per record:
 //
 //   a1/a2  the record (header + L/R flags + increment flags + bytes + packed
 //          attributes) is staged HBM -> shared memory with ONE TMA 1-D bulk copy
 //          (cp.async.bulk ... mbarrier::complete_tx), double-buffered per group so
 //          record i+1 is in flight while record i decodes;
-//   a3     index expansion: per-word __popc of the increment flags, an
-//          exclusive group scan over <= 8 words (__shfl), then
+//   a3     index expansion: per-word __popc of the increment flags, an exclusive group
+//          scan over the record's <= KW words (__shfl), then
 //          N[t+2] = i_t ? 2 + c_t : reuse[t - c_t - 1]      ("countbits");
 //   a4     L/R lookback by bit scan: j(t) = max{k<t: f_k != f_t} via
 //          31 - __clz((f_t ? ~w : w) & below(t)) in the current word, earlier words
 //          through per-word last-R / last-L max-scans ("firstbithigh");
 //   a5     triangle assembly with winding-preserving orientation (FORMAT.md §2);
-//   a6     index words stored directly (3 x u32 per lane, streaming .cs stores);
-//   a7/a8  attribute unpack (aligned halfwords at b = 16, else a bit reader),
+//   a6     index words stored directly (3 x u32 per lane, streaming .cs stores), or one
+//          local u8x4 word per triangle;
+//   a7/a8  attribute unpack (aligned halfwords at b = 16; compile-time shifts of word-aligned
+//          vertex units when every channel has one width; else a funnel-shift bit reader),
 //          q = L + code, fp32 via __fmaf_rn(__uint2float_rn(q), Δ, g),
 //          octahedral normals with IEEE-exact sqrt/reciprocal (FORMAT.md §4.3);
 //   a9     vertex words stored with 128-bit stores (direct when n_out % 4 == 0,
 //          else through the phase-aligned smem stage);
 //   a10    (stats kernel only) checksums/counters, group-reduced, one atomic per group.
 //
-// No tensor cores: the path is integer bit manipulation plus one FMA per
-// channel, bound by HBM bandwidth.  No --use_fast_math.
-// Compile-time tuning knobs (defaults are the measured optimum on B200, A/B tables in
-// profiles/experiments; scripts/build_variants.sh builds alternatives):
-//   MC_MIN_BLOCKS       __launch_bounds__ min blocks (default: 3 CTAs/SM = 80-register cap)
-//   MC_WORD_STEP        flag words per topology iteration with 16-lane groups (default 4:
-//                       every N[] of a T~ <= 128 meshlet first, one barrier, then every
-//                       triangle; the per-word broadcasts are shared by its two half-steps)
-//   MC_WORD_STEP32      the same for 32-lane groups (T~ > 128)
-//   MC_MAX_CTAS_PER_SM  cap on resident CTAs per SM used to size the persistent grid
-//   MC_GROUP16_TMAX     two meshlets per warp (16-lane groups) when T~ <= this
-//   MC_DYNAMIC          interleaved claim counters (0 = static grid stride)
-//   MC_STATIC_BELOW     launches with fewer records per group use the static-stride kernel (0 = never)
-//   MC_ST_CS            streaming (.cs) output stores
-//   MC_BANK_PAD         group smem stride = 16 (mod 32) words
+// No tensor cores: the path is integer bit manipulation plus one FMA per channel, bound by
+// HBM bandwidth.  No --use_fast_math.  Compile-time knobs (defaults = the
+// measured optimum on B200; A/B logs in profiles/experiments and profiles/round2/experiments;
+// scripts/build_variants.sh builds alternatives) are listed in decode_kernel.cuh.
 #include "decode_kernel.cuh"
 
 #include <cuda_runtime.h>
