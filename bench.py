@@ -420,7 +420,7 @@ def run_ours(args, rank, world, local_rank):
     view_dir = np.array([1.0, 2.0, -3.0], np.float64)
     view_dir = (view_dir / np.linalg.norm(view_dir)).astype(np.float32)
     stream = torch.cuda.Stream(dev)
-    if args.cull:   # FORMAT.md §7: one step = one-pass cull scan + decode of the visible records
+    if args.cull:   # FORMAT.md §7: one step = one-pass cull scan kernel + decode of the visible records
         step = lambda: db.decode_culled(view_dir)
         launches_per_step = 2
     else:

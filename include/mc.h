@@ -271,7 +271,8 @@ mc_status mc_decode_stats(const mc_decode_args *args, mc_stats *d_stats, void *s
  * first use: every completed call leaves its look-back flags and tile tickets zero again
  * (two calls in flight at the same time must not share one).  Asynchronous: two kernels
  * on `stream` — a one-pass cone test + decoupled look-back scan that lists the visible
- * records with their compacted output bases, then the decode kernel over that list.
+ * records with their compacted output bases, then the decode kernel over that list (a
+ * build with -DMC_CULL_FUSED=1 runs the scan inside the decode kernel: one launch).
  * Errors: MC_ERR_FORMAT (blob without cull table), MC_ERR_ARG, MC_ERR_LIMITS, MC_ERR_CUDA. */
 size_t mc_decode_culled_scratch_bytes(const mc_layout *layout);
 mc_status mc_decode_culled(const mc_decode_args *args, const float *view_dir, void *d_scratch, size_t scratch_bytes,

@@ -63,151 +63,23 @@ __global__ void stats_reset_kernel(mc_stats* s) {
 
 // ------------------------------------------------------------------ cone culling (FORMAT.md §1.5, §7)
 // The paper's amplification-shader pass: per record, the binary32 cone test
-// fmaf(az,dz, fmaf(ay,dy, ax*dx)) > cutoff and a one-pass decoupled look-back scan
-// (cull_scan_kernel) that lists the visible records in record order with their compacted
-// output bases.  The decode kernel then walks that list (Params::list): two launches.
-constexpr int kCullThreads = 256, kCullPerThread = 8, kCullTile = kCullThreads * kCullPerThread;
+// fmaf(az,dz, fmaf(ay,dy, ax*dx)) > cutoff and a one-pass decoupled look-back scan that
+// lists the visible records in record order with their compacted output bases
+// (cull_scan_tile, decode_kernel.cuh).  Default (MC_CULL_FUSED): the decode kernel runs the
+// scan itself before decoding the list — one launch.  Otherwise this standalone scan kernel
+// runs first and the decode kernel walks its list: two launches.
+constexpr uint32_t kCullThreads = 256, kCullTile = kCullThreads * kCullPerThread;
 
-struct CullParams {
-    const uint8_t* rec;
-    const uint32_t* dir;
-    const float4* cones;
-    uint64_t rec_section_bytes;
-    uint32_t M, vmax, tmax, max_rec;
-    float dx, dy, dz;
-    uint4* tile_agg;      // [tiles] tile totals {records, V, T', T} (look-back status 1)
-    uint4* tile_inc;      // [tiles] inclusive prefix through the tile (look-back status 2)
-    uint32_t* tile_flag;  // [tiles] 0 = not yet, 1 = aggregate published, 2 = inclusive published
-    uint32_t* ctr;        // [4]: tile ticket, CTAs done (zero at launch, left zero)
-    uint4* list;          // [M] {m, VB, TB, 0}
-    uint32_t* counts;     // [4] totals {records, V, T', T}
-    uint32_t tiles;
-};
-
-// visibility of record m and its counts (0 when not visible)
-__device__ __forceinline__ uint4 cull_one(const CullParams& C, uint32_t m) {
-    if (m >= C.M) return make_uint4(0, 0, 0, 0);
-    const uint32_t d0 = __ldg(C.dir + m), d1 = __ldg(C.dir + m + 1);
-    const uint64_t bytes = 16ull * (d1 - d0);
-    if (d1 <= d0 || bytes > C.max_rec || 16ull * d0 + bytes > C.rec_section_bytes) return make_uint4(0, 0, 0, 0);
-    const uint4 h = __ldg(reinterpret_cast<const uint4*>(C.rec + 16ull * d0));
-    const uint32_t V = (h.z & 0xFFu) + 1u, Tp = ((h.z >> 8) & 0xFFu) + 1u, R = h.w & 0xFFFFu;
-    if (V < 3u || V > C.vmax || Tp > C.tmax) return make_uint4(0, 0, 0, 0);
-    const float4 c = __ldg(C.cones + m);
-    const float sdot = __fmaf_rn(c.z, C.dz, __fmaf_rn(c.y, C.dy, __fmul_rn(c.x, C.dx)));
-    if (sdot > c.w) return make_uint4(0, 0, 0, 0);                     // culled: all back-facing
-    return make_uint4(1u, V, Tp, Tp - 4u * min(R, Tp / 4u));
-}
-
-__device__ __forceinline__ uint4 add4(uint4 a, uint4 b) { return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
-__device__ __forceinline__ uint4 shfl_up4(uint4 v, int d) {
-    return make_uint4(__shfl_up_sync(kFull, v.x, d), __shfl_up_sync(kFull, v.y, d), __shfl_up_sync(kFull, v.z, d),
-                      __shfl_up_sync(kFull, v.w, d));
-}
-// block-wide inclusive scan of one uint4 per thread (kCullThreads threads)
-__device__ __forceinline__ uint4 block_scan4(uint4 v, uint4* sh /* [kCullThreads/32] */) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint4 o = shfl_up4(v, d);
-        if (lane >= d) v = add4(v, o);
-    }
-    if (lane == 31) sh[wid] = v;
-    __syncthreads();
-    uint4 pre = make_uint4(0, 0, 0, 0);
-    for (int w = 0; w < wid; ++w) pre = add4(pre, sh[w]);
-    __syncthreads();
-    return add4(v, pre);
-}
-
-// One pass (a decoupled look-back scan, no host round trip, one launch): each CTA takes
-// the next tile of kCullTile records by ticket, tests its records, publishes the tile
-// total, looks back over the predecessors' published totals / inclusive prefixes for its
-// exclusive prefix, publishes its inclusive prefix and writes its visible records' list
-// entries {m, VB, TB} in record order.  The last tile writes the totals.  The last CTA to
-// finish clears the flags and tickets, so the scratch is zero again for the next call.
-__device__ __forceinline__ uint4 ld_volatile4(const uint4* p) {
-    const volatile uint32_t* q = reinterpret_cast<const volatile uint32_t*>(p);
-    return make_uint4(q[0], q[1], q[2], q[3]);
-}
-__device__ __forceinline__ void st_volatile4(uint4* p, uint4 v) {
-    volatile uint32_t* q = reinterpret_cast<volatile uint32_t*>(p);
-    q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
-}
-
-__global__ void __launch_bounds__(kCullThreads) cull_scan_kernel(const CullParams C) {
-    __shared__ uint4 sh[kCullThreads / 32];
+__global__ void __launch_bounds__(kCullThreads) cull_scan_kernel(const CullScan C) {
+    __shared__ uint4 sh[8], pair[2];
     __shared__ uint32_t s_tile, s_last;
-    __shared__ uint4 s_excl, s_agg;
     if (threadIdx.x == 0) s_tile = atomicAdd(C.ctr, 1u);     // tiles in CTA start order
     __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint32_t base = tile * kCullTile + threadIdx.x * kCullPerThread;
-    uint4 v[kCullPerThread];
-    uint4 acc = make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int i = 0; i < kCullPerThread; ++i) {
-        v[i] = cull_one(C, base + i);
-        acc = add4(acc, v[i]);
-    }
-    const uint4 inc = block_scan4(acc, sh);
-    if (threadIdx.x == kCullThreads - 1) s_agg = inc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint4 agg = s_agg;
-        uint4 excl = make_uint4(0, 0, 0, 0);
-        if (tile == 0) {
-            st_volatile4(C.tile_inc, agg);
-            __threadfence();
-            atomicExch(C.tile_flag, 2u);
-        } else {
-            st_volatile4(C.tile_agg + tile, agg);
-            __threadfence();
-            atomicExch(C.tile_flag + tile, 1u);
-            for (int j = (int)tile - 1; j >= 0; --j) {
-                uint32_t f;
-                while ((f = atomicAdd(C.tile_flag + j, 0u)) == 0u) {
-                }
-                __threadfence();
-                if (f == 2u) {
-                    excl = add4(excl, ld_volatile4(C.tile_inc + j));
-                    break;
-                }
-                excl = add4(excl, ld_volatile4(C.tile_agg + j));
-            }
-            st_volatile4(C.tile_inc + tile, add4(excl, agg));
-            __threadfence();
-            atomicExch(C.tile_flag + tile, 2u);
-        }
-        if (tile == C.tiles - 1) {
-            const uint4 tot = add4(excl, agg);
-            C.counts[0] = tot.x;
-            C.counts[1] = tot.y;
-            C.counts[2] = tot.z;
-            C.counts[3] = tot.w;
-        }
-        s_excl = excl;
-    }
-    __syncthreads();
-    uint4 run = add4(s_excl, make_uint4(inc.x - acc.x, inc.y - acc.y, inc.z - acc.z, inc.w - acc.w));
-#pragma unroll
-    for (int i = 0; i < kCullPerThread; ++i) {
-        if (v[i].x) C.list[run.x] = make_uint4(base + i, run.y, run.z, 0u);
-        run = add4(run, v[i]);
-    }
+    cull_scan_tile(C, s_tile, sh, pair);
     // leave the scratch zeroed: the last CTA clears flags and tickets
+    if (threadIdx.x == 0) s_last = atomicAdd(C.ctr + 2, 1u) == C.tiles - 1 ? 1u : 0u;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(C.ctr + 1, 1u) == C.tiles - 1 ? 1u : 0u;
-    }
-    __syncthreads();
-    if (s_last) {
-        for (uint32_t t = threadIdx.x; t < C.tiles; t += kCullThreads) C.tile_flag[t] = 0u;
-        if (threadIdx.x == 0) {
-            C.ctr[0] = 0u;
-            C.ctr[1] = 0u;
-        }
-    }
+    if (s_last) cull_scan_reset(C);
 }
 
 // ------------------------------------------------------------------ host launch
@@ -288,14 +160,21 @@ mc_status dispatch_codec(uint32_t codec, bool stats, int lay, int am, const Para
 }
 
 mc_status launch(const mc_decode_args* a, mc_stats* st, cudaStream_t s, const uint4* list = nullptr,
-                 const uint32_t* list_count = nullptr) {
+                 const uint32_t* list_count = nullptr, const CullScan* fused = nullptr) {
     Params P;
     size_t smem = 0;
     mc_status rc = build_params(a, st, P, smem);
     if (rc != MC_OK) return rc;
     P.list = list;
     P.list_count = list_count;
-    if (list) {   // culled decode: compacted outputs start at 0 (FORMAT.md §7)
+    P.cull_fused = 0;
+    if (fused) {   // one-launch culled decode: the kernel scans first (tiles set by launch_g)
+        P.cull_fused = 1;
+        P.cull = *fused;
+        P.list = fused->list;
+        P.list_count = fused->counts;
+    }
+    if (P.list) {   // culled decode: compacted outputs start at 0 (FORMAT.md §7)
         P.base_vtx = 0;
         P.base_tri = 0;
         P.index_sub = 0;
@@ -415,8 +294,10 @@ mc_status mc_decode_stats(const mc_decode_args* args, mc_stats* d_stats, void* s
 
 size_t mc_decode_culled_scratch_bytes(const mc_layout* L) {
     if (!L) return 0;
-    const uint64_t tiles = (uint64_t(L->num_meshlets) + kCullTile - 1) / kCullTile;
-    // list [M] uint4 | tile_agg [tiles] uint4 | tile_inc [tiles] uint4 | tile_flag [tiles] u32 | ctr [4] u32
+    // tiles of >= 32 threads x kCullPerThread records (the fused scan uses the decode CTA's
+    // warps, >= 1): list [M] uint4 | tile_agg [tiles] uint4 | tile_inc [tiles] uint4 |
+    // tile_flag [tiles] u32 | ctr [4] u32
+    const uint64_t tiles = (uint64_t(L->num_meshlets) + 32 * kCullPerThread - 1) / (32 * kCullPerThread);
     return size_t(16ull * L->num_meshlets + 32ull * tiles + ((4ull * tiles + 15) & ~15ull) + 16ull);
 }
 
@@ -434,7 +315,7 @@ mc_status mc_decode_culled(const mc_decode_args* a, const float* view_dir, void*
     if (!d_scratch || (reinterpret_cast<uintptr_t>(d_scratch) & 15u) || scratch_bytes < mc_decode_culled_scratch_bytes(&L))
         return MC_ERR_ARG;
     const uint8_t* blob = static_cast<const uint8_t*>(a->d_blob);
-    CullParams C;
+    CullScan C;
     C.rec = blob + L.off_rec;
     C.dir = reinterpret_cast<const uint32_t*>(blob + L.off_dir);
     C.cones = reinterpret_cast<const float4*>(blob + L.off_cull);
@@ -446,16 +327,22 @@ mc_status mc_decode_culled(const mc_decode_args* a, const float* view_dir, void*
     C.dx = view_dir[0];
     C.dy = view_dir[1];
     C.dz = view_dir[2];
-    C.tiles = (M + kCullTile - 1) / kCullTile;
+    const uint32_t max_tiles = (M + 32u * kCullPerThread - 1u) / (32u * kCullPerThread);
     C.list = static_cast<uint4*>(d_scratch);
     C.tile_agg = C.list + M;
-    C.tile_inc = C.tile_agg + C.tiles;
-    C.tile_flag = reinterpret_cast<uint32_t*>(C.tile_inc + C.tiles);
-    C.ctr = C.tile_flag + ((C.tiles + 3u) & ~3u);
+    C.tile_inc = C.tile_agg + max_tiles;
+    C.tile_flag = reinterpret_cast<uint32_t*>(C.tile_inc + max_tiles);
+    C.ctr = C.tile_flag + ((max_tiles + 3u) & ~3u);
     C.counts = d_counts;
+#if MC_CULL_FUSED
+    C.tiles = 0;   // launch_g sets it from the decode CTA size
+    return launch(a, d_stats, s, nullptr, nullptr, &C);
+#else
+    C.tiles = (M + kCullTile - 1) / kCullTile;
     cull_scan_kernel<<<C.tiles, kCullThreads, 0, s>>>(C);
     if (cudaGetLastError() != cudaSuccess) return MC_ERR_CUDA;
     return launch(a, d_stats, s, C.list, d_counts);
+#endif
 }
 
 mc_status mc_stats_reset(mc_stats* d_stats, void* stream) {
