@@ -126,6 +126,7 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     P.idx_stage_words = 0;
     P.idx = a->d_indices;
     P.fout = a->d_vertices;
+    P.fout32 = (reinterpret_cast<uintptr_t>(a->d_vertices) & 31u) == 0u;   // 256-bit vertex stores
     P.qout = a->d_quantized;
     P.stats = st;
     uint32_t off = 0, col = 0;
