@@ -221,7 +221,10 @@ typedef struct {
     uint32_t *d_indices;       /* device, required: 3*total_tp u32, FORMAT.md §2
                                   (positions relative to base_tri of the blob); total_tp
                                   u32 with MC_DECODE_INDEX_LOCAL_U8X4                      */
-    float *d_vertices;         /* device or NULL: n_out*total_v fp32, FORMAT.md §4.2       */
+    float *d_vertices;         /* device or NULL: n_out*total_v fp32, FORMAT.md §4.2;
+                                  16-B aligned (MC_ERR_ARG otherwise); with n_out = 8 a
+                                  32-B aligned buffer is written with one 256-bit store
+                                  per vertex (faster), a 16-B aligned one with two        */
     uint32_t *d_quantized;     /* device or NULL: n*total_v u32 grid values, §4.1          */
     uint32_t flags;            /* MC_DECODE_*                                             */
     uint32_t *d_work;          /* device or NULL: MC_DECODE_WORK_WORDS u32 of claim-counter

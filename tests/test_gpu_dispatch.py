@@ -120,3 +120,26 @@ def test_uniform_width_other_codecs(mc, orc, codec):
 def test_vw_kernels(mc, orc, codec, fmt):
     """Per-meshlet widths (FORMAT.md VW) at the dynamic launch size."""
     _check(mc, orc, _instanced(mc, "n7oct", codec, (64, 126), 60000, vw=True), fmt)
+
+
+@pytest.mark.parametrize("layout", ["n7oct", "n8"])
+def test_vertices_16b_aligned_output(mc, orc, layout):
+    """n_out = 8 vertices leave with one 256-bit store when d_vertices is 32-B aligned; a
+    buffer that is only 16-B aligned (the ABI's minimum) takes the two 128-bit stores.
+    Both at a dynamic-kernel launch size, element by element against the oracle."""
+    blob = _instanced(mc, layout, 2, (64, 126), 60_000)
+    data = np.array(blob.bytes)
+    L = blob.layout
+    d_blob = torch.from_numpy(data).cuda()
+    idx = torch.empty(3 * L.total_tp, dtype=torch.int32, device="cuda")
+    raw = torch.full((8 * L.total_v + 4,), float("nan"), dtype=torch.float32, device="cuda")
+    assert raw.data_ptr() % 32 == 0
+    err, errs, ridx, q, f = orc.decode(data, want_q=False)
+    assert err == 0
+    for off in (4, 0):                            # +16 B: not 32-B aligned; 0: aligned
+        verts = raw[off:off + 8 * L.total_v]
+        verts.fill_(float("nan"))
+        mc.mc_decode_meshlets(L, d_blob, idx, verts)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(idx.cpu().numpy().view(np.uint32), ridx)
+        np.testing.assert_array_equal(verts.cpu().numpy().view(np.uint32), f.view(np.uint32))
