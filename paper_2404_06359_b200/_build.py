@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmc.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = [os.path.join(CSRC, f) for f in ("encode.cpp", "decode.cu", "decode_inst.cu", "decode_kernel.cuh")] + \
+SOURCES = [os.path.join(CSRC, f) for f in ("encode.cpp", "decode.cu", "decode_inst.cu", "decode_kernel.cuh", "oct_math.cuh")] + \
           [os.path.join(ROOT, "include", "mc.h")]
 INSTS = [(c, st) for c in (1, 2, 3) for st in (0, 1)]
 
