@@ -17,7 +17,9 @@ import numpy as np
 
 from . import _build
 
-LIB_PATH = _build.LIB
+# MC_LIB: another build of the same library (tests/test_gpu_bounds.py loads the
+# bounds-checking build in a subprocess); default the in-tree product build
+LIB_PATH = os.environ.get("MC_LIB", _build.LIB)
 
 MC_CODEC_GTS, MC_CODEC_GTS_REUSE, MC_CODEC_BASIC = 1, 2, 3
 MC_DECODE_BLOB_LOCAL_INDICES, MC_DECODE_INDEX_LOCAL_U8X4 = 1, 2

@@ -73,8 +73,36 @@ def main():
         blob = mc.mc_blob_instance(protos, rng.integers(0, 3, n).astype(np.uint32),
                                    rng.uniform(-9, 9, (n, 3)).astype(np.float32))
         bad |= run(blob, stats=False) | run(blob, "u8x4", stats=False)
+    if "--fuzz" in sys.argv:
+        fuzz()
     print("decode error bits:", bad)
     sys.exit(1 if bad else 0)
+
+
+def fuzz(rounds: int = 40):
+    """Random byte corruption inside the records section (header and directory intact, so
+    the blob parses): every kernel must stay inside its buffers whatever the records hold
+    (error bits are expected and not counted)."""
+    rng = np.random.default_rng(7)
+    blobs = [mc.mc_encode(synth.quad_grid(32, 32), 64, 126, c) for c in (1, 2, 3)]
+    blobs += [mc.mc_encode(synth.quad_grid(24, 24, bits=12), 32, 32, 2),
+              mc.mc_encode(synth.random_patch(3, nx=30, ny=20), 128, 256, 2),
+              mc.mc_encode(synth.quad_grid(32, 32), 64, 126, 2, variable_widths=True)]
+    for r in range(rounds):
+        src = blobs[r % len(blobs)]
+        data = np.array(src.bytes).copy()
+        L = src.layout
+        lo = int(L.off_rec)
+        k = int(rng.integers(1, 64))
+        pos = rng.integers(lo, data.size, k)
+        data[pos] ^= rng.integers(1, 256, k).astype(np.uint8)
+        blob = mc.Blob.from_bytes(data)
+        for fmt in ("u32", "u8x4"):
+            db = mc.DeviceBlob(blob, want_vertices=True, want_quantized=True, index_format=fmt)
+            db.decode()
+            db.decode_stats()
+    torch.cuda.synchronize()
+    print("fuzz rounds:", rounds)
 
 
 if __name__ == "__main__":
