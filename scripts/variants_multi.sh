@@ -13,7 +13,7 @@ for so in build_var/libmc_*.so; do
     timeout 300 $B $wa 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$name', '$wn', round(d['value'],2), round(d['roofline']['frac'],3), d['checksum']['error_bits'], 'step_ms', d.get('step_ms',{}).get('median'), 'mhz', d.get('clocks',{}).get('sm_mhz'), d.get('clocks',{}).get('reasons'))"
   done
   [ -n "$NOSWEEP" ] && continue
-  timeout 600 python scripts/sweep_cfg5.py --out /tmp/sw_$name.jsonl --sizes 32x32,64x64 --bits 16,10 --label $name > /dev/null 2>&1
+  timeout 900 python scripts/sweep_cfg5.py --instances ${SWEEP_INST:-100} --out /tmp/sw_$name.jsonl --sizes 32x32,64x64 --bits 16,10 --label $name > /dev/null 2>&1
   python -c "
 import json
 for l in open('/tmp/sw_$name.jsonl'):
