@@ -127,6 +127,8 @@ mc_status build_params(const mc_decode_args* a, mc_stats* st, Params& P, size_t&
     P.idx = a->d_indices;
     P.fout = a->d_vertices;
     P.fout32 = (reinterpret_cast<uintptr_t>(a->d_vertices) & 31u) == 0u;   // 256-bit vertex stores
+    P.pair16 = 1;   // every channel at most 16 bits wide (VW widths w_c <= b_c)
+    for (uint32_t c = 0; c < L.n; ++c) P.pair16 &= L.bits[c] <= 16u ? 1u : 0u;
     P.qout = a->d_quantized;
     P.stats = st;
     uint32_t off = 0, col = 0;
