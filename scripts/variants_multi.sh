@@ -9,7 +9,7 @@ for so in build_var/libmc_*.so; do
   cp $so paper_2404_06359_b200/libmc.so
   name=$(basename $so .so)
   for w in ${WLS:-"cfg4:" "cfg4u8:--index-format u8x4" "shard8:--instances 125" "vw:--variable-widths"}; do
-    wn=${w%%:*}; wa=${w#*:}
+    wn=${w%%:*}; wa=${w#*:}; wa=${wa//,/ }
     timeout 300 $B $wa 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$name', '$wn', round(d['value'],2), round(d['roofline']['frac'],3), d['checksum']['error_bits'], 'step_ms', d.get('step_ms',{}).get('median'), 'mhz', d.get('clocks',{}).get('sm_mhz'), d.get('clocks',{}).get('reasons'))"
   done
   [ -n "$NOSWEEP" ] && continue
